@@ -1,0 +1,136 @@
+/*
+ * bfsht-b200 C ABI.
+ *
+ * Drop-in boundary for the apply phase of the reference package `bfsht`
+ * (arXiv 2004.11346).  The reference has no FFI; its boundary is the set of
+ * Python apply functions, which paper_2004_11346_b200/api.py mirrors with the
+ * same names, argument meaning and ValueError messages on top of this ABI:
+ *
+ *   reference (pkg/src/bfsht/…)                 replaced by
+ *   ------------------------------------------  ---------------------------------
+ *   alt.py:264  alt_forward(plan, coeffs)        bfsht_alt_apply(.., BFSHT_FORWARD)
+ *   alt.py:275  alt_inverse(plan, column)        bfsht_alt_apply(.., BFSHT_INVERSE)
+ *   alt.py:197  _apply_half  (+ butterfly.py:275
+ *               idbf_apply, lowrank.py:196)      stages of bfsht_alt_apply
+ *   alt.py:211  _apply_half_transpose (+ :285
+ *               idbf_apply_transpose, :200)      stages of bfsht_alt_apply
+ *   sht.py:137  sht_forward(plan, coeffs)         bfsht_sht_forward
+ *   sht.py:151  sht_inverse(plan, grid_values)    bfsht_sht_inverse
+ *   sht.py:148,161 np.fft.ifft/fft(axis=1)       bfsht_dft_rows
+ *   alt.py:57 AltPlan / butterfly.py:66 payloads  bfsht_pack_plan (host) +
+ *                                                bfsht_plan_upload (device)
+ *
+ * Conventions: plain pointers and sizes only; device pointers are raw CUDA
+ * device addresses, `stream` is a cudaStream_t passed as void*.  Every call
+ * returns 0 on success or a negative code, with a message retrievable from
+ * bfsht_last_error() (thread-local).  Device buffers created by the library
+ * are owned by the handle; pointers passed in are borrowed.
+ */
+#ifndef BFSHT_B200_H
+#define BFSHT_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BFSHT_FORWARD 0
+#define BFSHT_INVERSE 1
+
+/* ---------------------------------------------------------------- host side
+ * Plan manifest: the reference payload layout, flattened.  One entry per
+ * retained block of every AltPlan half (pkg/src/bfsht/alt.py:57-73,
+ * partition.py:189-204).  kind: 0 butterfly (butterfly.py:66-80, COO
+ * factors, factors[0] applied first), 1 low-rank u diag(s) v^T
+ * (lowrank.py:184-202), 2 dense h x w row-major (alt.py:183-187). */
+typedef struct {
+    int32_t order;              /* index into bfsht_manifest.m            */
+    int32_t parity;             /* 0 odd, 1 even                          */
+    int32_t kind;
+    int32_t r0, r1, c0, c1;     /* Block.trim                             */
+    int32_t rank;               /* low-rank r                             */
+    const double *a, *b, *c;    /* dense: a; low-rank: u, s, v            */
+    int32_t nfac, levels, middle;
+    const int64_t *fshape;      /* 2*nfac                                 */
+    const int64_t *fnnz;        /* nfac                                   */
+    const int64_t *const *frows;
+    const int64_t *const *fcols;
+    const double *const *fvals;
+} bfsht_block;
+
+typedef struct {
+    int32_t n;                  /* transform half-size N (2N nodes)       */
+    int32_t norders;
+    const int32_t *m;           /* order of each plan                     */
+    const int32_t *ncols;       /* 2*norders: (odd, even) columns, 0=absent */
+    int64_t nblocks;
+    const bfsht_block *blocks;
+} bfsht_manifest;
+
+typedef struct bfsht_packed bfsht_packed;   /* opaque host-side packed plan */
+
+/* Pack a manifest into the device format (tiles + task lists).  Threads:
+ * 0 = all host cores.  Returns 0 / negative. */
+int bfsht_pack_plan(const bfsht_manifest *man, int threads,
+                    bfsht_packed **out);
+/* Sizes and host pointers of the packed arrays (for upload / inspection).
+ * info[]: 0 tile doubles, 1 ops, 2 idx, 3 lane maps, 4 tasks,
+ * 5 arena entries, 6 halves, 7 stages fwd, 8 stages inv,
+ * 9 payload values (sum of stored reference values), 10 stored tile doubles
+ * incl. zero fill, 11 butterfly blocks, 12 low-rank blocks, 13 dense blocks,
+ * 14 half-size N, 15 number of order plans */
+int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]);
+int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]);
+void bfsht_packed_free(bfsht_packed *p);
+
+const char *bfsht_last_error(void);
+
+/* ------------------------------------------------------------- device side */
+typedef struct bfsht_plan bfsht_plan;       /* opaque device plan */
+
+/* Upload a packed plan (arrays as returned by bfsht_packed_arrays) to the
+ * current device. */
+int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out);
+/* Device arrays already resident (e.g. allocated through torch), borrowed:
+ * dev[0..5] = tiles, ops, idx, maps, tasks, halves (bfsht_packed_arrays
+ * order), dev[6] = vector arena (info[5] x 4 doubles); host[5..7] = host
+ * copies of halves and the two stage-bound arrays. */
+int bfsht_plan_wrap(const int64_t info[16], const void *const host[8],
+                    void *const dev[8], bfsht_plan **out);
+void bfsht_plan_free(bfsht_plan *pl);
+/* Device pointer to the vector arena (info[5] entries x 4 doubles). */
+double *bfsht_plan_arena(bfsht_plan *pl);
+
+/* Run every ALT stage of one direction over the arena (inputs already in
+ * the arena: coefficient halves for FORWARD, node halves for INVERSE). */
+int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream);
+
+/* Per-order ALT boundary (alt_forward / alt_inverse for one or more plans):
+ * in/out are device complex128 buffers laid out plan after plan, lengths
+ * 2N-m (coefficients) and 2N (node values); weights = 2N quadrature
+ * weights (device) for the inverse fold (alt.py:239-253). */
+int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
+                     const double *weights, void *stream);
+
+/* Full SHT on device buffers.  coeffs: flat m-major complex128, m from
+ * -(2N-1) to 2N-1 (ShtCoeffs.pack(), sht.py:68-81); grid: 2N x (4N-1)
+ * complex128 row-major, rows node-ascending.  The plan must hold orders
+ * 0..2N-1 in order. */
+int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid,
+                      void *stream);
+int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
+                      const double *weights, void *stream);
+
+/* Batched length-L complex DFT of `rows` contiguous rows, unnormalized,
+ * sign -1 (dir FORWARD, numpy fft) or +1 (INVERSE, L*ifft). */
+int bfsht_dft_rows(int64_t L, int64_t rows, int dir, const double *in,
+                   double *out, void *stream);
+
+/* Number of kernel launches issued by the last apply on this plan. */
+int64_t bfsht_plan_launches(bfsht_plan *pl);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

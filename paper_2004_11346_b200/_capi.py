@@ -1,0 +1,51 @@
+"""ctypes declarations for libbfsht_b200.so (include/bfsht_b200.h)."""
+import ctypes
+
+from . import pack
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int
+_I64 = ctypes.c_int64
+
+
+def declare(lib):
+    pack.declare(lib)
+    lib.bfsht_last_error.restype = ctypes.c_char_p
+    lib.bfsht_last_error.argtypes = []
+    lib.bfsht_plan_upload.restype = _I
+    lib.bfsht_plan_upload.argtypes = [_P, ctypes.POINTER(_P)]
+    lib.bfsht_plan_wrap.restype = _I
+    lib.bfsht_plan_wrap.argtypes = [ctypes.POINTER(_I64), ctypes.POINTER(_P),
+                                    ctypes.POINTER(_P), ctypes.POINTER(_P)]
+    lib.bfsht_plan_free.restype = None
+    lib.bfsht_plan_free.argtypes = [_P]
+    lib.bfsht_plan_arena.restype = _P
+    lib.bfsht_plan_arena.argtypes = [_P]
+    lib.bfsht_plan_launches.restype = _I64
+    lib.bfsht_plan_launches.argtypes = [_P]
+    lib.bfsht_alt_apply.restype = _I
+    lib.bfsht_alt_apply.argtypes = [_P, _I, _P]
+    lib.bfsht_alt_orders.restype = _I
+    lib.bfsht_alt_orders.argtypes = [_P, _I, _P, _P, _P, _P]
+    lib.bfsht_sht_forward.restype = _I
+    lib.bfsht_sht_forward.argtypes = [_P, _P, _P, _P]
+    lib.bfsht_sht_inverse.restype = _I
+    lib.bfsht_sht_inverse.argtypes = [_P, _P, _P, _P, _P]
+    lib.bfsht_dft_rows.restype = _I
+    lib.bfsht_dft_rows.argtypes = [_I64, _I64, _I, _P, _P, _P]
+
+
+# every symbol include/bfsht_b200.h declares (checked by tests on CPU)
+EXPORTS = (
+    "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
+    "bfsht_packed_free", "bfsht_last_error", "bfsht_plan_upload",
+    "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
+    "bfsht_alt_apply", "bfsht_alt_orders", "bfsht_sht_forward",
+    "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
+)
+
+
+def check(lib, rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed ({rc}): "
+                           f"{lib.bfsht_last_error().decode()}")

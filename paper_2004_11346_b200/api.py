@@ -1,0 +1,332 @@
+"""Apply path on the B200: the reference's apply API over the C ABI.
+
+Same names, argument meaning and ValueError messages as the reference
+(pkg/src/bfsht/alt.py:264-282, sht.py:137-166):
+
+    alt_forward(plan, coeffs)        -> GridFunctionColumn
+    alt_inverse(plan, column)        -> CoeffVector
+    sht_forward(plan, coeffs)        -> ShtGridValues
+    sht_inverse(plan, grid_values)   -> ShtCoeffs
+
+``plan`` is an ``AltPlan`` / ``ShtPlan`` in the reference layout (from
+``plan_alt`` / ``plan_sht`` of this package, or from ``bfsht``).  On first
+use the plan is packed (csrc/packer.cpp) and uploaded once; the device
+plan is cached on the plan object.  Host numpy inputs return host numpy
+outputs like the reference; CUDA torch tensors stay on the device.
+
+``DevicePlan`` is the lower-level handle (device arrays owned by torch, the
+C ABI borrows them); ``ShtDevice`` runs whole transforms on device tensors.
+There is no CPU fallback: without the CUDA library or a GPU every call
+raises.
+"""
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from ._capi import check
+from .pack import NRHS, pack_plans
+from .sht import ShtCoeffs, ShtGridValues
+
+FORWARD, INVERSE = 0, 1
+
+
+@dataclass
+class CoeffVector:
+    """Coefficients for degrees k = m .. 2N-1, ascending; length 2N - m."""
+
+    m: int
+    values: np.ndarray
+
+
+@dataclass
+class GridFunctionColumn:
+    """One order's profile at the 2N quadrature angles, node-ascending."""
+
+    m: int
+    values: np.ndarray
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2004_11346_b200 needs a CUDA device "
+                           "(no CPU fallback)")
+    return torch
+
+
+def _stream_ptr(torch, stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class DevicePlan:
+    """A packed plan resident on one GPU.
+
+    Device arrays (tile store, ops, indices, lane maps, tasks, halves, and
+    the vector arena) are torch tensors; the native handle borrows them.
+    """
+
+    def __init__(self, plans, device=None, packed=None, weights=None):
+        torch = _torch()
+        self.lib = native.cuda()
+        plans = list(plans)
+        self.packed = pack_plans(plans) if packed is None else packed
+        pk = self.packed
+        self.n = pk.n
+        self.orders = [int(m) for m in pk.orders]
+        self.device = torch.device("cuda", torch.cuda.current_device()
+                                   if device is None else device)
+        with torch.cuda.device(self.device):
+            def up(a, dtype=None):
+                t = torch.from_numpy(np.ascontiguousarray(a))
+                if dtype is not None:
+                    t = t.view(dtype)
+                return t.to(self.device)
+
+            self._dev = [
+                up(pk.tiles if pk.tiles.size else np.zeros(2)),
+                up(pk.ops.view(np.uint8) if pk.ops.size else np.zeros(24, np.uint8)),
+                up(pk.idx if pk.idx.size else np.zeros(1, np.int32)),
+                up(pk.maps if pk.maps.size else np.zeros(32, np.int8)),
+                up(pk.tasks.view(np.int32) if pk.tasks.size else np.zeros(4, np.int32)),
+                up(pk.halves.view(np.int32)),
+            ]
+            self.arena = torch.zeros((max(pk.stats["arena"], 1), NRHS),
+                                     dtype=torch.float64, device=self.device)
+            if weights is None and plans:
+                weights = plans[0].quadrature.weights
+            self.weights = None if weights is None else \
+                torch.as_tensor(np.asarray(weights, dtype=np.float64),
+                                device=self.device)
+            self._host_halves = np.ascontiguousarray(pk.halves)
+            self._sf = np.ascontiguousarray(pk.stages_fwd)
+            self._si = np.ascontiguousarray(pk.stages_inv)
+            info = (ctypes.c_int64 * 16)(*[int(v) for v in pk.info])
+            host = (ctypes.c_void_p * 8)()
+            host[5] = self._host_halves.ctypes.data
+            host[6] = self._sf.ctypes.data
+            host[7] = self._si.ctypes.data
+            dev = (ctypes.c_void_p * 8)()
+            for i, t in enumerate(self._dev):
+                dev[i] = t.data_ptr()
+            dev[6] = self.arena.data_ptr()
+            h = ctypes.c_void_p()
+            check(self.lib, self.lib.bfsht_plan_wrap(info, host, dev,
+                                                     ctypes.byref(h)),
+                  "bfsht_plan_wrap")
+            self.handle = h
+        self.coeff_len = sum(2 * self.n - m for m in self.orders)
+
+    # ---------------------------------------------------------------- stats
+    @property
+    def stats(self):
+        return self.packed.stats
+
+    def payload_bytes(self):
+        return self.packed.payload_bytes()
+
+    def launches(self):
+        return int(self.lib.bfsht_plan_launches(self.handle))
+
+    # -------------------------------------------------------------- apply
+    def alt_apply(self, direction, stream=None):
+        """All ALT stages over the arena (inputs already in place)."""
+        torch = _torch()
+        check(self.lib, self.lib.bfsht_alt_apply(
+            self.handle, direction, _stream_ptr(torch, stream)), "bfsht_alt_apply")
+
+    def alt_orders(self, direction, inp, out=None, stream=None):
+        """Per-order ALT on device complex128 tensors laid out plan after
+        plan: forward in = coefficients (2N-m each), out = 2N node values;
+        inverse the reverse."""
+        torch = _torch()
+        n2 = 2 * self.n
+        inp = inp.contiguous()
+        if out is None:
+            size = len(self.orders) * n2 if direction == FORWARD else self.coeff_len
+            out = torch.empty(size, dtype=torch.complex128, device=self.device)
+        w = self.weights.data_ptr() if self.weights is not None else None
+        check(self.lib, self.lib.bfsht_alt_orders(
+            self.handle, direction, ctypes.c_void_p(inp.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
+            _stream_ptr(torch, stream)), "bfsht_alt_orders")
+        return out
+
+    def sht_forward(self, coeffs, out=None, stream=None):
+        torch = _torch()
+        n = self.n
+        if out is None:
+            out = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128,
+                              device=self.device)
+        check(self.lib, self.lib.bfsht_sht_forward(
+            self.handle, ctypes.c_void_p(coeffs.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), _stream_ptr(torch, stream)),
+            "bfsht_sht_forward")
+        return out
+
+    def sht_inverse(self, grid, out=None, stream=None):
+        torch = _torch()
+        n = self.n
+        if out is None:
+            out = torch.empty(4 * n * n, dtype=torch.complex128, device=self.device)
+        check(self.lib, self.lib.bfsht_sht_inverse(
+            self.handle, ctypes.c_void_p(grid.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(self.weights.data_ptr()),
+            _stream_ptr(torch, stream)), "bfsht_sht_inverse")
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.bfsht_plan_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _device_plan(plan):
+    dp = getattr(plan, "_b200_device_plan", None)
+    if dp is None:
+        dp = DevicePlan([plan])
+        try:
+            plan._b200_device_plan = dp
+        except AttributeError:
+            pass
+    return dp
+
+
+def _as_device(torch, values, dp):
+    is_tensor = isinstance(values, torch.Tensor)
+    if is_tensor:
+        return values.to(dp.device, torch.complex128), True, values.is_complex()
+    arr = np.asarray(values)
+    cplx = np.iscomplexobj(arr)
+    return torch.from_numpy(np.ascontiguousarray(arr, dtype=np.complex128)) \
+        .to(dp.device), False, cplx
+
+
+def _shape_of(values):
+    return tuple(values.shape)
+
+
+def alt_forward(plan, coeffs):
+    """Coefficients beta_k (k = m..2N-1) to values at the 2N nodes
+    (reference alt.py:264-272)."""
+    values = coeffs.values if isinstance(coeffs, CoeffVector) else coeffs
+    if not hasattr(values, "shape"):
+        values = np.asarray(values)
+    if _shape_of(values) != (2 * plan.n - plan.m,):
+        raise ValueError(f"expected {2 * plan.n - plan.m} coefficients, "
+                         f"got shape {_shape_of(values)}")
+    torch = _torch()
+    dp = _device_plan(plan)
+    x, on_dev, cplx = _as_device(torch, values, dp)
+    y = dp.alt_orders(FORWARD, x)
+    if not on_dev:
+        y = y.cpu().numpy()
+        if not cplx:
+            y = y.real.copy()
+    elif not cplx:
+        y = y.real.contiguous()
+    return GridFunctionColumn(m=plan.m, values=y)
+
+
+def alt_inverse(plan, column):
+    """Values at the 2N nodes back to coefficients via the weighted
+    transpose (reference alt.py:275-282)."""
+    values = column.values if isinstance(column, GridFunctionColumn) else column
+    if not hasattr(values, "shape"):
+        values = np.asarray(values)
+    if _shape_of(values) != (2 * plan.n,):
+        raise ValueError(f"expected {2 * plan.n} node values, "
+                         f"got shape {_shape_of(values)}")
+    torch = _torch()
+    dp = _device_plan(plan)
+    x, on_dev, cplx = _as_device(torch, values, dp)
+    y = dp.alt_orders(INVERSE, x)
+    if not on_dev:
+        y = y.cpu().numpy()
+        if not cplx:
+            y = y.real.copy()
+    elif not cplx:
+        y = y.real.contiguous()
+    return CoeffVector(m=plan.m, values=y)
+
+
+class ShtDevice:
+    """Whole-transform handle: every order's plan resident on one GPU."""
+
+    def __init__(self, sht_plan, device=None):
+        self.n = sht_plan.n
+        ms = [p.m for p in sht_plan.alt_plans]
+        if ms != list(range(2 * self.n)):
+            raise ValueError("ShtPlan must hold plans for m = 0..2N-1")
+        self.plan = DevicePlan(sht_plan.alt_plans, device=device,
+                               weights=sht_plan.quadrature.weights)
+
+    def forward(self, coeffs, out=None, stream=None):
+        return self.plan.sht_forward(coeffs, out, stream)
+
+    def inverse(self, grid, out=None, stream=None):
+        return self.plan.sht_inverse(grid, out, stream)
+
+
+def _sht_device(plan):
+    dev = getattr(plan, "_b200_sht_device", None)
+    if dev is None:
+        dev = ShtDevice(plan)
+        try:
+            plan._b200_sht_device = dev
+        except AttributeError:
+            pass
+    return dev
+
+
+def sht_forward(plan, coeffs):
+    """Coefficients to grid values f(theta_l, phi_j), shape 2N x (4N-1)
+    (reference sht.py:137-148)."""
+    n = plan.n
+    if coeffs.n != n:
+        raise ValueError(f"coefficient set is for N={coeffs.n}, plan N={n}")
+    torch = _torch()
+    dev = _sht_device(plan)
+    flat = torch.from_numpy(np.ascontiguousarray(coeffs.pack(),
+                                                 dtype=np.complex128))
+    grid = dev.forward(flat.to(dev.plan.device))
+    return ShtGridValues(n=n, values=grid.cpu().numpy())
+
+
+def sht_inverse(plan, grid_values):
+    """Grid values to coefficients (reference sht.py:151-166)."""
+    n = plan.n
+    values = grid_values.values if isinstance(grid_values, ShtGridValues) \
+        else np.asarray(grid_values)
+    if values.shape != (2 * n, 4 * n - 1):
+        raise ValueError(f"expected grid shape {(2 * n, 4 * n - 1)}, "
+                         f"got {values.shape}")
+    torch = _torch()
+    dev = _sht_device(plan)
+    g = torch.from_numpy(np.ascontiguousarray(values, dtype=np.complex128))
+    flat = dev.inverse(g.to(dev.plan.device))
+    return ShtCoeffs.unpack(n, flat.cpu().numpy())
+
+
+def dft_rows(x, inverse=False, stream=None):
+    """Batched length-L DFT of the rows of a complex128 CUDA tensor:
+    numpy fft(axis=1) (forward) or L*ifft(axis=1) (inverse)."""
+    torch = _torch()
+    lib = native.cuda()
+    x = x.contiguous()
+    out = torch.empty_like(x)
+    rows, L = x.shape
+    check(lib, lib.bfsht_dft_rows(L, rows, INVERSE if inverse else FORWARD,
+                                  ctypes.c_void_p(x.data_ptr()),
+                                  ctypes.c_void_p(out.data_ptr()),
+                                  _stream_ptr(torch, stream)), "bfsht_dft_rows")
+    return out

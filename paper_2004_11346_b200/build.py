@@ -58,7 +58,8 @@ def build_cuda(force=False):
     srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
                   if f.endswith(".cu"))
     heads = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
-             if f.endswith(".cuh")] + [os.path.join(INCLUDE, "bfsht_b200.h")]
+             if f.endswith((".cuh", ".h", ".cpp"))] + [
+        os.path.join(INCLUDE, "bfsht_b200.h")]
     if not srcs:
         return None
     if not force and not _stale(out, srcs + [h for h in heads
@@ -71,7 +72,13 @@ def build_cuda(force=False):
                               "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                               "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj])
         objs.append(obj)
-    _run([NVCC] + ARCH + ["-shared", "-o", out] + objs)
+    # the packer rides along so C users get pack + upload + apply in one .so
+    pk = os.path.join(CSRC, "packer.cpp")
+    pobj = os.path.join(CSRC, "packer.cuda.o")
+    _run(["g++", "-O3", "-fPIC", "-std=c++17", "-fopenmp", "-I", INCLUDE,
+          "-c", pk, "-o", pobj])
+    objs.append(pobj)
+    _run([NVCC] + ARCH + ["-shared", "-o", out] + objs + ["-lgomp"])
     return out
 
 

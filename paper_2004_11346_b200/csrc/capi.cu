@@ -1,0 +1,223 @@
+// extern "C" entry points of libbfsht_b200.so (declared in
+// include/bfsht_b200.h).  Plain pointers and sizes; no torch types.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bfsht_b200.h"
+#include "engine.cuh"
+
+static thread_local std::string g_err;
+
+void bfsht_set_error(const std::string &msg) { g_err = msg; }
+
+int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStream_t st);
+int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const double *weights,
+                   cudaStream_t st);
+int bf_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out, const double *weights,
+                  cudaStream_t st);
+int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *in, double *out,
+                cudaStream_t st);
+
+namespace {
+
+int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
+                const int64_t *si) {
+    const int64_t nh = pl->info[6];
+    pl->stages[0].assign(sf, sf + pl->info[7] + 1);
+    pl->stages[1].assign(si, si + pl->info[8] + 1);
+    pl->norders = (int32_t)(nh / 2);
+    pl->n = (int32_t)pl->info[14];
+    pl->orders.resize(pl->norders);
+    std::vector<int64_t> off(pl->norders + 1, 0);
+    for (int o = 0; o < pl->norders; ++o) {
+        pl->orders[o] = host_halves[2 * o].m;
+        off[o + 1] = off[o] + 2 * (int64_t)pl->n - pl->orders[o];
+    }
+    BF_CUDA(cudaMalloc(&pl->order_off, sizeof(int64_t) * (pl->norders + 1)));
+    pl->owned.push_back(pl->order_off);
+    BF_CUDA(cudaMemcpy(pl->order_off, off.data(), sizeof(int64_t) * (pl->norders + 1),
+                       cudaMemcpyHostToDevice));
+    pl->ncounters = (int)std::max(pl->info[7], pl->info[8]) + 1;
+    BF_CUDA(cudaMalloc(&pl->counters, sizeof(int) * pl->ncounters));
+    pl->owned.push_back(pl->counters);
+    int dev = 0;
+    BF_CUDA(cudaGetDevice(&dev));
+    BF_CUDA(cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev));
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *bfsht_last_error(void) { return g_err.c_str(); }
+
+int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
+    if (!p || !out) {
+        g_err = "null argument";
+        return -1;
+    }
+    auto *pl = new bfsht_plan();
+    if (bfsht_packed_info(p, pl->info)) {
+        delete pl;
+        g_err = "bad packed plan";
+        return -1;
+    }
+    const void *arr[8];
+    bfsht_packed_arrays(p, arr);
+    const size_t sz[6] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
+                          (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_T,
+                          (size_t)pl->info[4] * sizeof(bf_task),
+                          (size_t)pl->info[6] * sizeof(bf_half)};
+    void *dev[6];
+    for (int i = 0; i < 6; ++i) {
+        dev[i] = nullptr;
+        if (cudaMalloc(&dev[i], sz[i] ? sz[i] : 16) != cudaSuccess ||
+            (sz[i] && cudaMemcpy(dev[i], arr[i], sz[i], cudaMemcpyHostToDevice) != cudaSuccess)) {
+            g_err = "device allocation/copy failed";
+            for (int j = 0; j <= i; ++j) cudaFree(dev[j]);
+            delete pl;
+            return -2;
+        }
+        pl->owned.push_back(dev[i]);
+    }
+    void *arena = nullptr;
+    if (cudaMalloc(&arena, (size_t)pl->info[5] * BF_NRHS * 8 + 16) != cudaSuccess) {
+        g_err = "arena allocation failed";
+        bfsht_plan_free(pl);
+        return -2;
+    }
+    pl->owned.push_back(arena);
+    pl->tiles = (const double *)dev[0];
+    pl->ops = (const bf_op *)dev[1];
+    pl->idx = (const int32_t *)dev[2];
+    pl->maps = (const int8_t *)dev[3];
+    pl->tasks = (const bf_task *)dev[4];
+    pl->halves = (const bf_half *)dev[5];
+    pl->arena = (double *)arena;
+    int rc = finish_plan(pl, (const bf_half *)arr[5], (const int64_t *)arr[6],
+                         (const int64_t *)arr[7]);
+    if (rc) {
+        bfsht_plan_free(pl);
+        return rc;
+    }
+    *out = pl;
+    return 0;
+}
+
+int bfsht_plan_wrap(const int64_t info[16], const void *const host[8], void *const dev[8],
+                    bfsht_plan **out) {
+    if (!info || !host || !dev || !out) {
+        g_err = "null argument";
+        return -1;
+    }
+    auto *pl = new bfsht_plan();
+    std::memcpy(pl->info, info, sizeof(pl->info));
+    pl->tiles = (const double *)dev[0];
+    pl->ops = (const bf_op *)dev[1];
+    pl->idx = (const int32_t *)dev[2];
+    pl->maps = (const int8_t *)dev[3];
+    pl->tasks = (const bf_task *)dev[4];
+    pl->halves = (const bf_half *)dev[5];
+    pl->arena = (double *)dev[6];
+    int rc = finish_plan(pl, (const bf_half *)host[5], (const int64_t *)host[6],
+                         (const int64_t *)host[7]);
+    if (rc) {
+        bfsht_plan_free(pl);
+        return rc;
+    }
+    *out = pl;
+    return 0;
+}
+
+void bfsht_plan_free(bfsht_plan *pl) {
+    if (!pl) return;
+    for (void *p : pl->owned) cudaFree(p);
+    for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
+                    (void *)pl->dft_scratch})
+        if (p) cudaFree(p);
+    delete pl;
+}
+
+double *bfsht_plan_arena(bfsht_plan *pl) { return pl ? pl->arena : nullptr; }
+
+int64_t bfsht_plan_launches(bfsht_plan *pl) { return pl ? pl->launches : -1; }
+
+int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream) {
+    if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan or direction";
+        return -1;
+    }
+    pl->launches = 0;
+    return bf_alt_apply(pl, dir, (cudaStream_t)stream);
+}
+
+int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
+                     const double *weights, void *stream) {
+    if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan or direction";
+        return -1;
+    }
+    if (dir == BFSHT_INVERSE && !weights) {
+        g_err = "inverse ALT needs quadrature weights";
+        return -1;
+    }
+    pl->launches = 0;
+    return bf_alt_orders(pl, dir, in, out, weights, (cudaStream_t)stream);
+}
+
+static int check_sht(bfsht_plan *pl) {
+    if (!pl) {
+        g_err = "null plan";
+        return -1;
+    }
+    if (pl->norders != 2 * pl->n) {
+        g_err = "SHT needs plans for every order m = 0..2N-1";
+        return -1;
+    }
+    for (int o = 0; o < pl->norders; ++o)
+        if (pl->orders[o] != o) {
+            g_err = "SHT plans must be ordered by m";
+            return -1;
+        }
+    return 0;
+}
+
+int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, void *stream) {
+    if (check_sht(pl)) return -1;
+    pl->launches = 0;
+    return bf_sht_forward(pl, coeffs, grid, (cudaStream_t)stream);
+}
+
+int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
+                      const double *weights, void *stream) {
+    if (check_sht(pl)) return -1;
+    if (!weights) {
+        g_err = "inverse SHT needs quadrature weights";
+        return -1;
+    }
+    pl->launches = 0;
+    return bf_sht_inverse(pl, grid, coeffs, weights, (cudaStream_t)stream);
+}
+
+int bfsht_dft_rows(int64_t L, int64_t rows, int dir, const double *in, double *out,
+                   void *stream) {
+    static thread_local bfsht_plan *scratch_plan = nullptr;
+    if (L < 1 || rows < 0 || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad DFT arguments";
+        return -1;
+    }
+    if (!scratch_plan) {
+        scratch_plan = new bfsht_plan();
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&scratch_plan->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return bf_dft_rows(scratch_plan, L, rows, dir, in, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

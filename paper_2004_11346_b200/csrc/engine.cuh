@@ -1,0 +1,59 @@
+// Device-side plan handle and launch helpers shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bfsht_b200.h"
+#include "format.h"
+
+struct bfsht_plan {
+    int64_t info[16];
+    const double *tiles = nullptr;
+    const bf_op *ops = nullptr;
+    const int32_t *idx = nullptr;
+    const int8_t *maps = nullptr;
+    const bf_task *tasks = nullptr;
+    const bf_half *halves = nullptr;
+    double *arena = nullptr;
+    std::vector<int64_t> stages[2];   // task bounds per stage (host)
+    int32_t n = 0;                    // half size N
+    int32_t norders = 0;
+    std::vector<int32_t> orders;      // m of each plan (host)
+    // owned device allocations (upload path) and scratch
+    std::vector<void *> owned;
+    int *counters = nullptr;          // one per stage launch (device)
+    int ncounters = 0;
+    // per-order API scratch
+    int64_t *order_off = nullptr;     // device, 2*norders+2 offsets
+    // DFT tables (built lazily for L = 4N-1)
+    int64_t dft_L = 0;
+    double *dft_w = nullptr;          // L complex: exp(-2 pi i k / L)
+    int32_t *dft_perm = nullptr;      // digit-reversal positions
+    double *dft_tw = nullptr;         // L complex: exp(i m phi0) per bin
+    std::vector<int32_t> dft_radix;
+    double *dft_scratch = nullptr;    // global fallback buffer
+    int64_t dft_scratch_rows = 0;
+    int64_t launches = 0;
+    int sm_count = 148;
+};
+
+void bfsht_set_error(const std::string &msg);
+
+#define BF_CUDA(call)                                                          \
+    do {                                                                       \
+        cudaError_t _e = (call);                                               \
+        if (_e != cudaSuccess) {                                               \
+            bfsht_set_error(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+            return -2;                                                         \
+        }                                                                      \
+    } while (0)
+
+// engine.cu
+int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter,
+                 cudaStream_t s);
+int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
+// sht.cu
+int bf_dft_prepare(bfsht_plan *pl, int64_t L);

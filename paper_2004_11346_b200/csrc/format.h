@@ -1,0 +1,67 @@
+/*
+ * Device plan format shared by the host packer (packer.cpp) and the CUDA
+ * apply engine (engine.cu).  Plain C so it can sit under the C ABI.
+ *
+ * Every payload value of a plan (dense turning blocks, low-rank u*diag(s)
+ * and v, butterfly ID interpolation blocks and middle skeleton blocks)
+ * lives in one fp64 "tile store" as R x C tiles (R, C <= 32), each tile
+ * contiguous and 16-byte aligned, element (r, c) at c*R + (r + c) % R.
+ * That rotation makes both tile products conflict-free from shared memory:
+ *   N-mode  lane r: sum_c A[r][c] * v[c]   (apply)
+ *   T-mode  lane c: sum_r A[r][c] * v[r]   (apply transpose)
+ * so one stored copy serves the forward ALT (A x) and the inverse ALT
+ * (A^T y) — the reference's "one plan serves both directions"
+ * (pkg/src/bfsht/alt.py:1-9).
+ *
+ * All vectors (coefficient halves, node halves, butterfly intermediates,
+ * low-rank cores, butterfly block outputs) live in one "vector arena" of
+ * NRHS-double entries addressed by int32 entry index; NRHS = 4 carries
+ * (Re, Im) of +m and -m, which share one plan (pkg/src/bfsht/sht.py:146).
+ *
+ * A task produces <= 32 consecutive arena entries as a fixed-order sum of
+ * ops, so results are deterministic run to run (no atomics).  Tasks are
+ * grouped in stages; a stage only reads entries written by earlier stages.
+ */
+#ifndef BFSHT_FORMAT_H
+#define BFSHT_FORMAT_H
+#include <stdint.h>
+
+#define BF_T 32          /* max tile edge / outputs per task */
+#define BF_NRHS 4        /* doubles per arena entry */
+
+enum bf_op_kind {
+    BF_OP_TILE_N = 0,    /* lanes = tile rows, inputs = C entries  */
+    BF_OP_TILE_T = 1,    /* lanes = tile cols, inputs = R entries  */
+    BF_OP_ADD = 2        /* lanes [off, off+R) += arena[src]       */
+};
+
+enum bf_op_flags {
+    BF_OPF_GATHER = 1,   /* inputs through idx[in + i], else in + i (idx < 0: none) */
+    BF_OPF_LANEMAP = 2   /* outputs through maps[aux*32 + slot] (tile lane or -1) */
+};
+
+typedef struct {
+    int64_t tile;        /* element offset of the tile in the tile store  */
+    int32_t in;          /* arena entry (contiguous) or idx offset (gather) */
+    int32_t aux;         /* lane-map index when BF_OPF_LANEMAP            */
+    uint8_t kind, R, C, off;
+    uint8_t flags, pad0;
+    uint16_t pad1;
+} bf_op;                 /* 24 bytes */
+
+typedef struct {
+    int32_t op_begin;
+    int32_t op_count;
+    int32_t out;         /* first arena entry written */
+    int32_t nout;        /* entries written (<= 32) */
+} bf_task;               /* 16 bytes */
+
+/* per (order, parity) half: where its vectors live */
+typedef struct {
+    int32_t x;           /* coefficient half: ncols entries (fwd in, inv out) */
+    int32_t y;           /* node half: n entries (fwd out, inv in)            */
+    int32_t ncols;       /* 0 when this parity half is absent                 */
+    int32_t m;
+} bf_half;
+
+#endif

@@ -1,0 +1,715 @@
+// Host packer: reference-layout plan payloads -> device tile store + tasks.
+//
+// Input is the reference payload layout (pkg/src/bfsht/alt.py:57-73,
+// butterfly.py:45-80, lowrank.py:184-202) flattened into a bfsht_manifest.
+// Output is the format of format.h.  Nothing is approximated: every stored
+// reference value lands in exactly one tile (plus explicit zeros where a
+// dense block or ID tile has structural zeros), and the per-task op order
+// fixes the summation order.
+//
+// Block kinds and how they become tasks (forward / inverse):
+//  * dense turning block P: tiles cut on the absolute 32-row / 32-column
+//    grid of its half matrix; N-mode ops in the row-group task of the node
+//    half (forward, alt.py:207) and T-mode ops in the column-group task of
+//    the coefficient half (inverse, alt.py:221).
+//  * low-rank u diag(s) v^T (lowrank.py:196-202): s folded into u; a stage-0
+//    task forms t = v^T x (fwd) or t = (u s)^T y (inv), the group tasks add
+//    (u s) t or v t.
+//  * butterfly chain (butterfly.py:275-292): every factor is put in its
+//    "ID orientation" G (G = F for the V factors and the middle, G = F^T for
+//    the U factors, whose COO is the transpose of a column ID,
+//    butterfly.py:153-157).  G's rows are split into segments of rows that
+//    share column support (one segment = one interpolative decomposition);
+//    in a segment, columns holding a single exact 1.0 are identity
+//    ("skeleton") entries and become index adds, the rest form a dense
+//    interpolation block.  Applying G is a gather task per 32 segment rows
+//    (N-mode tiles); applying G^T is a scatter task per 32 output columns
+//    of the segment's column range (T-mode tiles through a lane map), with
+//    all segments sharing a range summed in one task.  The same tiles serve
+//    both, so a factor is stored once.  Depth-0 chains are dense blocks.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <omp.h>
+
+#include "bfsht_b200.h"
+#include "format.h"
+
+static thread_local std::string g_err;
+
+extern "C" const char *bfsht_host_last_error(void) { return g_err.c_str(); }
+
+struct bfsht_packed {
+    std::unique_ptr<double[]> tiles;
+    int64_t n_tiles = 0;
+    std::vector<bf_op> ops;
+    std::vector<int32_t> idx;
+    std::vector<int8_t> maps;
+    std::vector<bf_task> tasks;
+    std::vector<bf_half> halves;
+    std::vector<int64_t> stage_bounds[2];
+    int64_t arena = 0;
+    int64_t payload_values = 0;
+    int64_t n_bf = 0, n_lr = 0, n_dn = 0;
+    int64_t n = 0, norders = 0;
+};
+
+namespace {
+
+struct TileJob {
+    int64_t dst;
+    int R, C;
+    const double *src;
+    int64_t rs, cs;  // element (r, c) = src[r*rs + c*cs]
+};
+
+struct TaskBuild {
+    int32_t out, nout;
+    std::vector<bf_op> ops;
+    double cost = 0.0;
+};
+
+// One interpolative decomposition (segment of G rows).
+struct Segment {
+    int64_t row0, rows;          // G rows [row0, row0+rows)
+    std::vector<int64_t> dcols;  // dense columns, ascending
+    std::vector<double> t;       // rows x dcols.size(), row-major
+    std::vector<std::pair<int64_t, int64_t>> units;  // (row, col)
+    int64_t cmin = -1, cmax = -1;
+    int range = -1;
+};
+
+struct FactorSegs {
+    int64_t nrows = 0, ncols = 0;              // G shape
+    std::vector<Segment> segs;
+    std::vector<std::pair<int64_t, int64_t>> ranges;  // [a, b) covering [0, ncols)
+    std::vector<int> range_has_segs;
+};
+
+std::vector<std::pair<int64_t, int64_t>> cuts(int64_t a, int64_t b) {
+    // [a, b) cut at absolute multiples of BF_T
+    std::vector<std::pair<int64_t, int64_t>> out;
+    int64_t x = a;
+    while (x < b) {
+        int64_t nx = std::min<int64_t>(b, (x / BF_T + 1) * BF_T);
+        out.push_back({x, nx});
+        x = nx;
+    }
+    return out;
+}
+
+// Split G (given as COO in G orientation) into ID segments.
+void segment_factor(int64_t nr, int64_t nc, int64_t nnz, const int64_t *gr,
+                    const int64_t *gc, const double *gv, FactorSegs &fs) {
+    fs.nrows = nr;
+    fs.ncols = nc;
+    // CSR by row, columns ascending within a row
+    std::vector<int64_t> rowptr(nr + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) {
+        if (gr[e] < 0 || gr[e] >= nr || gc[e] < 0 || gc[e] >= nc)
+            throw std::runtime_error("factor triplet index out of range");
+        rowptr[gr[e] + 1]++;
+    }
+    for (int64_t r = 0; r < nr; ++r) rowptr[r + 1] += rowptr[r];
+    std::vector<int64_t> ccol(nnz);
+    std::vector<double> cval(nnz);
+    {
+        std::vector<int64_t> fill(rowptr.begin(), rowptr.end() - 1);
+        for (int64_t e = 0; e < nnz; ++e) {
+            int64_t p = fill[gr[e]]++;
+            ccol[p] = gc[e];
+            cval[p] = gv[e];
+        }
+        std::vector<std::pair<int64_t, double>> tmp;
+        for (int64_t r = 0; r < nr; ++r) {
+            int64_t b = rowptr[r], e = rowptr[r + 1];
+            if (e - b < 2) continue;
+            tmp.clear();
+            for (int64_t p = b; p < e; ++p) tmp.push_back({ccol[p], cval[p]});
+            std::sort(tmp.begin(), tmp.end(),
+                      [](auto &x, auto &y) { return x.first < y.first; });
+            for (int64_t p = b; p < e; ++p) {
+                ccol[p] = tmp[p - b].first;
+                cval[p] = tmp[p - b].second;
+            }
+        }
+    }
+    // greedy segmentation on shared support
+    std::vector<int64_t> stamp(nc, -1);
+    std::vector<std::pair<int64_t, int64_t>> bounds;
+    int64_t cur = -1, start = 0;
+    bool cur_dense = false;
+    for (int64_t r = 0; r < nr; ++r) {
+        int64_t b = rowptr[r], e = rowptr[r + 1];
+        bool unit_row = (e - b == 1 && cval[b] == 1.0);
+        bool fresh;
+        if (cur < 0) {
+            fresh = true;
+        } else if (e == b) {
+            fresh = false;
+        } else {
+            int64_t overlap = 0;
+            for (int64_t p = b; p < e; ++p) overlap += (stamp[ccol[p]] == cur);
+            fresh = overlap == 0 && !(unit_row && !cur_dense);
+        }
+        if (fresh) {
+            if (cur >= 0) bounds.push_back({start, r});
+            cur = (int64_t)bounds.size();
+            start = r;
+            cur_dense = false;
+        }
+        for (int64_t p = b; p < e; ++p) stamp[ccol[p]] = cur;
+        if (e > b && !unit_row) cur_dense = true;
+    }
+    if (nr > 0) bounds.push_back({start, nr});
+
+    std::vector<int32_t> cnt(nc, 0);
+    std::vector<double> lastv(nc, 0.0);
+    std::vector<int64_t> lastr(nc, -1), pos(nc, -1);
+    for (auto &bd : bounds) {
+        Segment s;
+        s.row0 = bd.first;
+        s.rows = bd.second - bd.first;
+        std::vector<int64_t> touched;
+        for (int64_t r = bd.first; r < bd.second; ++r)
+            for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+                int64_t c = ccol[p];
+                if (cnt[c] == 0) touched.push_back(c);
+                cnt[c]++;
+                lastv[c] = cval[p];
+                lastr[c] = r;
+            }
+        std::sort(touched.begin(), touched.end());
+        for (int64_t c : touched) {
+            if (cnt[c] == 1 && lastv[c] == 1.0)
+                s.units.push_back({lastr[c], c});
+            else
+                s.dcols.push_back(c);
+        }
+        if (!touched.empty()) {
+            s.cmin = touched.front();
+            s.cmax = touched.back();
+        }
+        for (size_t j = 0; j < s.dcols.size(); ++j) pos[s.dcols[j]] = (int64_t)j;
+        const int64_t nd = (int64_t)s.dcols.size();
+        s.t.assign((size_t)(s.rows * nd), 0.0);
+        for (int64_t r = bd.first; r < bd.second; ++r)
+            for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) {
+                int64_t c = ccol[p];
+                if (!(cnt[c] == 1 && lastv[c] == 1.0))
+                    s.t[(size_t)((r - bd.first) * nd + pos[c])] = cval[p];
+            }
+        for (int64_t c : touched) {
+            cnt[c] = 0;
+            pos[c] = -1;
+        }
+        fs.segs.push_back(std::move(s));
+    }
+    // column ranges: merged support intervals, gaps filled, covering [0, nc)
+    std::vector<std::pair<int64_t, int64_t>> iv;
+    for (auto &s : fs.segs)
+        if (s.cmin >= 0) iv.push_back({s.cmin, s.cmax + 1});
+    std::sort(iv.begin(), iv.end());
+    std::vector<std::pair<int64_t, int64_t>> merged;
+    for (auto &x : iv) {
+        if (!merged.empty() && x.first < merged.back().second)
+            merged.back().second = std::max(merged.back().second, x.second);
+        else
+            merged.push_back(x);
+    }
+    int64_t at = 0;
+    for (auto &x : merged) {
+        if (x.first > at) {
+            fs.ranges.push_back({at, x.first});
+            fs.range_has_segs.push_back(0);
+        }
+        fs.ranges.push_back(x);
+        fs.range_has_segs.push_back(1);
+        at = x.second;
+    }
+    if (at < nc) {
+        fs.ranges.push_back({at, nc});
+        fs.range_has_segs.push_back(0);
+    }
+    for (auto &s : fs.segs) {
+        if (s.cmin < 0) continue;
+        auto it = std::upper_bound(
+            fs.ranges.begin(), fs.ranges.end(), std::make_pair(s.cmin, INT64_MAX));
+        s.range = (int)(it - fs.ranges.begin()) - 1;
+    }
+}
+
+struct Packer {
+    bfsht_packed &P;
+    const bfsht_manifest &M;
+    std::vector<TileJob> jobs;
+    std::vector<std::unique_ptr<std::vector<double>>> keep;  // temp sources
+    // tasks by direction and stage
+    std::vector<std::vector<TaskBuild>> stages[2];
+    // per half: group ops (fwd row groups over Y, inv col groups over X)
+    std::vector<std::vector<std::vector<bf_op>>> fwd_groups, inv_groups;
+
+    Packer(bfsht_packed &p, const bfsht_manifest &m) : P(p), M(m) {}
+
+    int32_t alloc_entries(int64_t n) {
+        int64_t at = P.arena;
+        P.arena += n;
+        if (P.arena > INT32_MAX) throw std::runtime_error("vector arena exceeds int32");
+        return (int32_t)at;
+    }
+    int64_t alloc_tile(int R, int C, const double *src, int64_t rs, int64_t cs) {
+        int64_t at = P.n_tiles;
+        P.n_tiles += ((int64_t)R * C + 1) & ~int64_t(1);
+        jobs.push_back({at, R, C, src, rs, cs});
+        return at;
+    }
+    std::vector<TaskBuild> &stage(int dir, int s) {
+        if ((int)stages[dir].size() <= s) stages[dir].resize(s + 1);
+        return stages[dir][s];
+    }
+    static bf_op mk(int kind, int64_t tile, int32_t in, int R, int C, int off,
+                    int flags = 0, int32_t aux = 0) {
+        bf_op o;
+        std::memset(&o, 0, sizeof(o));
+        o.tile = tile;
+        o.in = in;
+        o.aux = aux;
+        o.kind = (uint8_t)kind;
+        o.R = (uint8_t)R;
+        o.C = (uint8_t)C;
+        o.off = (uint8_t)off;
+        o.flags = (uint8_t)flags;
+        return o;
+    }
+    static double op_cost(const bf_op &o) {
+        if (o.kind == BF_OP_ADD) return 32.0 * o.R;
+        return 8.0 * o.R * o.C + 32.0 * (o.kind == BF_OP_TILE_N ? o.C : o.R);
+    }
+    int32_t push_idx(const std::vector<int32_t> &v) {
+        int64_t at = (int64_t)P.idx.size();
+        P.idx.insert(P.idx.end(), v.begin(), v.end());
+        if ((int64_t)P.idx.size() > INT32_MAX) throw std::runtime_error("idx exceeds int32");
+        return (int32_t)at;
+    }
+    int32_t push_map(const int8_t *m) {
+        int64_t at = (int64_t)P.maps.size() / BF_T;
+        P.maps.insert(P.maps.end(), m, m + BF_T);
+        return (int32_t)at;
+    }
+    void add_task(int dir, int s, int32_t out, int32_t nout, std::vector<bf_op> &&ops) {
+        TaskBuild t;
+        t.out = out;
+        t.nout = nout;
+        for (auto &o : ops) t.cost += op_cost(o);
+        t.ops = std::move(ops);
+        stage(dir, s).push_back(std::move(t));
+    }
+
+    // ---------------------------------------------------------- dense
+    void dense(int h_idx, const double *a, int64_t lda, int64_t r0, int64_t r1,
+               int64_t c0, int64_t c1) {
+        const bf_half &hf = P.halves[h_idx];
+        for (auto rr : cuts(r0, r1))
+            for (auto cc : cuts(c0, c1)) {
+                int R = (int)(rr.second - rr.first), C = (int)(cc.second - cc.first);
+                int64_t t = alloc_tile(R, C, a + (rr.first - r0) * lda + (cc.first - c0), lda, 1);
+                int g = (int)(rr.first / BF_T), gc = (int)(cc.first / BF_T);
+                fwd_groups[h_idx][g].push_back(mk(BF_OP_TILE_N, t, hf.x + (int32_t)cc.first, R, C,
+                                                  (int)(rr.first - (int64_t)g * BF_T)));
+                inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, C,
+                                                   (int)(cc.first - (int64_t)gc * BF_T)));
+            }
+    }
+
+    // -------------------------------------------------------- low-rank
+    void lowrank(int h_idx, const bfsht_block &b) {
+        const bf_half &hf = P.halves[h_idx];
+        const int64_t h = b.r1 - b.r0, w = b.c1 - b.c0, r = b.rank;
+        if (r <= 0) return;
+        auto us = std::make_unique<std::vector<double>>((size_t)(h * r));
+        for (int64_t i = 0; i < h; ++i)
+            for (int64_t k = 0; k < r; ++k) (*us)[i * r + k] = b.a[i * r + k] * b.b[k];
+        const double *u = us->data();
+        keep.push_back(std::move(us));
+        const double *v = b.c;
+        int32_t tf = alloc_entries(r), ti = alloc_entries(r);
+        for (int64_t k0 = 0; k0 < r; k0 += BF_T) {
+            int K = (int)std::min<int64_t>(BF_T, r - k0);
+            std::vector<bf_op> f1, i1;
+            for (auto cc : cuts(b.c0, b.c1)) {  // v tiles: rows = block columns
+                int R = (int)(cc.second - cc.first);
+                int64_t t = alloc_tile(R, K, v + (cc.first - b.c0) * r + k0, r, 1);
+                f1.push_back(mk(BF_OP_TILE_T, t, hf.x + (int32_t)cc.first, R, K, 0));
+                int gc = (int)(cc.first / BF_T);
+                inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_N, t, ti + (int32_t)k0, R, K,
+                                                   (int)(cc.first - (int64_t)gc * BF_T)));
+            }
+            for (auto rr : cuts(b.r0, b.r1)) {  // u s tiles: rows = block rows
+                int R = (int)(rr.second - rr.first);
+                int64_t t = alloc_tile(R, K, u + (rr.first - b.r0) * r + k0, r, 1);
+                i1.push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, K, 0));
+                int g = (int)(rr.first / BF_T);
+                fwd_groups[h_idx][g].push_back(mk(BF_OP_TILE_N, t, tf + (int32_t)k0, R, K,
+                                                  (int)(rr.first - (int64_t)g * BF_T)));
+            }
+            add_task(0, 0, tf + (int32_t)k0, K, std::move(f1));
+            add_task(1, 0, ti + (int32_t)k0, K, std::move(i1));
+        }
+        (void)h;
+        (void)w;
+    }
+
+    // ---------------------------------------------------- butterfly
+    // gather tasks applying G: in_vec indexes G columns, out_vec G rows
+    void gather_tasks(const FactorSegs &fs, std::vector<std::vector<int64_t>> &tile_of,
+                      int dir, int st, int32_t in_vec, int32_t out_vec) {
+        for (size_t si = 0; si < fs.segs.size(); ++si) {
+            const Segment &s = fs.segs[si];
+            const auto &runs = tile_runs(fs, s);
+            for (int64_t p0 = 0, p = 0; p0 < s.rows; p0 += BF_T, ++p) {
+                int R = (int)std::min<int64_t>(BF_T, s.rows - p0);
+                std::vector<bf_op> ops;
+                for (size_t q = 0; q < runs.size(); ++q) {
+                    int C = (int)(runs[q].second - runs[q].first);
+                    std::vector<int32_t> ix(C);
+                    for (int c = 0; c < C; ++c)
+                        ix[c] = in_vec + (int32_t)s.dcols[runs[q].first + c];
+                    ops.push_back(mk(BF_OP_TILE_N, tile_of[si][p * runs.size() + q], push_idx(ix),
+                                     R, C, 0, BF_OPF_GATHER));
+                }
+                // identity (skeleton) entries; a row may carry more than one
+                std::vector<std::vector<int32_t>> lanes;
+                for (auto &u : s.units) {
+                    int64_t lr = u.first - s.row0 - p0;
+                    if (lr < 0 || lr >= R) continue;
+                    size_t k = 0;
+                    while (k < lanes.size() && lanes[k][lr] >= 0) ++k;
+                    if (k == lanes.size()) lanes.emplace_back(BF_T, -1);
+                    lanes[k][lr] = in_vec + (int32_t)u.second;
+                }
+                for (auto &ln : lanes) {
+                    ln.resize(R);
+                    ops.push_back(mk(BF_OP_ADD, 0, push_idx(ln), R, 0, 0, BF_OPF_GATHER));
+                }
+                add_task(dir, st, out_vec + (int32_t)(s.row0 + p0), R, std::move(ops));
+            }
+        }
+    }
+
+    // column runs of a segment's dense columns cut at 32-chunks of its range
+    std::vector<std::pair<int64_t, int64_t>> tile_runs(const FactorSegs &fs, const Segment &s) {
+        std::vector<std::pair<int64_t, int64_t>> runs;
+        if (s.dcols.empty()) return runs;
+        const int64_t a = fs.ranges[s.range].first;
+        int64_t b = 0;
+        for (int64_t j = 1; j <= (int64_t)s.dcols.size(); ++j) {
+            if (j == (int64_t)s.dcols.size() ||
+                (s.dcols[j] - a) / BF_T != (s.dcols[b] - a) / BF_T) {
+                runs.push_back({b, j});
+                b = j;
+            }
+        }
+        return runs;
+    }
+
+    // scatter tasks applying G^T: in_vec indexes G rows, out_vec G columns
+    void scatter_tasks(const FactorSegs &fs, std::vector<std::vector<int64_t>> &tile_of,
+                       int dir, int st, int32_t in_vec, int32_t out_vec) {
+        std::vector<std::vector<size_t>> by_range(fs.ranges.size());
+        for (size_t si = 0; si < fs.segs.size(); ++si)
+            if (fs.segs[si].range >= 0) by_range[fs.segs[si].range].push_back(si);
+        for (size_t ri = 0; ri < fs.ranges.size(); ++ri) {
+            const int64_t a = fs.ranges[ri].first, e = fs.ranges[ri].second;
+            for (int64_t q0 = a; q0 < e; q0 += BF_T) {
+                const int64_t qid = (q0 - a) / BF_T;
+                int nout = (int)std::min<int64_t>(BF_T, e - q0);
+                std::vector<bf_op> ops;
+                for (size_t si : by_range[ri]) {
+                    const Segment &s = fs.segs[si];
+                    const auto runs = tile_runs(fs, s);
+                    for (size_t q = 0; q < runs.size(); ++q) {
+                        if ((s.dcols[runs[q].first] - a) / BF_T != qid) continue;
+                        int C = (int)(runs[q].second - runs[q].first);
+                        int8_t lm[BF_T];
+                        std::memset(lm, -1, sizeof(lm));
+                        for (int c = 0; c < C; ++c)
+                            lm[s.dcols[runs[q].first + c] - q0] = (int8_t)c;
+                        int32_t mi = push_map(lm);
+                        for (int64_t p0 = 0, p = 0; p0 < s.rows; p0 += BF_T, ++p) {
+                            int R = (int)std::min<int64_t>(BF_T, s.rows - p0);
+                            ops.push_back(mk(BF_OP_TILE_T, tile_of[si][p * runs.size() + q],
+                                             in_vec + (int32_t)(s.row0 + p0), R, C, 0,
+                                             BF_OPF_LANEMAP, mi));
+                        }
+                    }
+                    std::vector<int32_t> ln(nout, -1);
+                    bool any = false;
+                    for (auto &u : s.units) {
+                        if (u.second < q0 || u.second >= q0 + nout) continue;
+                        ln[u.second - q0] = in_vec + (int32_t)u.first;
+                        any = true;
+                    }
+                    if (any) ops.push_back(mk(BF_OP_ADD, 0, push_idx(ln), nout, 0, 0, BF_OPF_GATHER));
+                }
+                add_task(dir, st, out_vec + (int32_t)q0, nout, std::move(ops));
+            }
+        }
+    }
+
+    void butterfly(int h_idx, const bfsht_block &b, std::vector<FactorSegs> &segs) {
+        const bf_half &hf = P.halves[h_idx];
+        const int L = b.nfac;
+        const int64_t h = b.r1 - b.r0, w = b.c1 - b.c0;
+        const int nv = 1 + b.levels - b.middle;
+        // forward vectors z[0..L], inverse vectors zi[0..L]
+        std::vector<int32_t> z(L + 1), zi(L + 1);
+        z[0] = hf.x + b.c0;
+        for (int i = 1; i < L; ++i) z[i] = alloc_entries(b.fshape[2 * (i - 1)]);
+        z[L] = alloc_entries(h);
+        zi[0] = hf.y + b.r0;
+        for (int j = 1; j < L; ++j) zi[j] = alloc_entries(b.fshape[2 * (L - j) + 1]);
+        zi[L] = alloc_entries(w);
+        for (int i = 0; i < L; ++i) {
+            FactorSegs &fs = segs[i];
+            bool g_is_f = i <= nv;
+            // tiles of every segment: row groups x column runs
+            std::vector<std::vector<int64_t>> tile_of(fs.segs.size());
+            for (size_t si = 0; si < fs.segs.size(); ++si) {
+                const Segment &s = fs.segs[si];
+                auto runs = tile_runs(fs, s);
+                const int64_t nd = (int64_t)s.dcols.size();
+                for (int64_t p0 = 0; p0 < s.rows; p0 += BF_T)
+                    for (auto &rn : runs) {
+                        int R = (int)std::min<int64_t>(BF_T, s.rows - p0);
+                        int C = (int)(rn.second - rn.first);
+                        tile_of[si].push_back(alloc_tile(R, C, s.t.data() + p0 * nd + rn.first, nd, 1));
+                    }
+            }
+            if (g_is_f) {
+                gather_tasks(fs, tile_of, 0, i, z[i], z[i + 1]);
+                scatter_tasks(fs, tile_of, 1, L - 1 - i, zi[L - 1 - i], zi[L - i]);
+            } else {
+                scatter_tasks(fs, tile_of, 0, i, z[i], z[i + 1]);
+                gather_tasks(fs, tile_of, 1, L - 1 - i, zi[L - 1 - i], zi[L - i]);
+            }
+        }
+        // block outputs into the group tasks
+        for (auto rr : cuts(b.r0, b.r1)) {
+            int g = (int)(rr.first / BF_T);
+            fwd_groups[h_idx][g].push_back(mk(BF_OP_ADD, 0, z[L] + (int32_t)(rr.first - b.r0),
+                                              (int)(rr.second - rr.first), 0,
+                                              (int)(rr.first - (int64_t)g * BF_T)));
+        }
+        for (auto cc : cuts(b.c0, b.c1)) {
+            int gc = (int)(cc.first / BF_T);
+            inv_groups[h_idx][gc].push_back(mk(BF_OP_ADD, 0, zi[L] + (int32_t)(cc.first - b.c0),
+                                               (int)(cc.second - cc.first), 0,
+                                               (int)(cc.first - (int64_t)gc * BF_T)));
+        }
+    }
+
+    void run(int threads) {
+        const int n = M.n;
+        // halves and their arena vectors
+        P.halves.resize((size_t)M.norders * 2);
+        fwd_groups.resize(P.halves.size());
+        inv_groups.resize(P.halves.size());
+        for (int o = 0; o < M.norders; ++o)
+            for (int par = 0; par < 2; ++par) {
+                bf_half &hf = P.halves[o * 2 + par];
+                hf.m = M.m[o];
+                hf.ncols = M.ncols[o * 2 + par];
+                if (hf.ncols > 0) {
+                    hf.x = alloc_entries(hf.ncols);
+                    hf.y = alloc_entries(n);
+                    fwd_groups[o * 2 + par].resize((n + BF_T - 1) / BF_T);
+                    inv_groups[o * 2 + par].resize((hf.ncols + BF_T - 1) / BF_T);
+                } else {
+                    hf.x = hf.y = -1;
+                }
+            }
+        // butterfly segmentation in parallel (the heavy part)
+        std::vector<std::vector<FactorSegs>> segs((size_t)M.nblocks);
+        std::vector<std::string> errs((size_t)M.nblocks);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+        for (int64_t bi = 0; bi < M.nblocks; ++bi) {
+            const bfsht_block &b = M.blocks[bi];
+            if (b.kind != 0 || b.nfac < 2) continue;
+            try {
+                const int nv = 1 + b.levels - b.middle;
+                segs[bi].resize(b.nfac);
+                for (int i = 0; i < b.nfac; ++i) {
+                    bool g_is_f = i <= nv;
+                    int64_t fr = b.fshape[2 * i], fc = b.fshape[2 * i + 1];
+                    if (g_is_f)
+                        segment_factor(fr, fc, b.fnnz[i], b.frows[i], b.fcols[i], b.fvals[i], segs[bi][i]);
+                    else
+                        segment_factor(fc, fr, b.fnnz[i], b.fcols[i], b.frows[i], b.fvals[i], segs[bi][i]);
+                }
+            } catch (std::exception &e) {
+                errs[bi] = e.what();
+            }
+        }
+        for (int64_t bi = 0; bi < M.nblocks; ++bi)
+            if (!errs[bi].empty())
+                throw std::runtime_error("block " + std::to_string(bi) + ": " + errs[bi]);
+
+        for (int64_t bi = 0; bi < M.nblocks; ++bi) {
+            const bfsht_block &b = M.blocks[bi];
+            if (b.order < 0 || b.order >= M.norders || b.parity < 0 || b.parity > 1)
+                throw std::runtime_error("block order/parity out of range");
+            const int h_idx = b.order * 2 + b.parity;
+            const bf_half &hf = P.halves[h_idx];
+            if (hf.ncols <= 0) throw std::runtime_error("block in an absent half");
+            if (b.r0 < 0 || b.r1 > n || b.r0 >= b.r1 || b.c0 < 0 || b.c1 > hf.ncols || b.c0 >= b.c1)
+                throw std::runtime_error("block trim outside its half");
+            const int64_t h = b.r1 - b.r0, w = b.c1 - b.c0;
+            if (b.kind == 2) {
+                P.n_dn++;
+                P.payload_values += h * w;
+                dense(h_idx, b.a, w, b.r0, b.r1, b.c0, b.c1);
+            } else if (b.kind == 1) {
+                P.n_lr++;
+                P.payload_values += (h + w + 1) * (int64_t)b.rank;
+                lowrank(h_idx, b);
+            } else if (b.kind == 0) {
+                P.n_bf++;
+                int64_t vals = 0;
+                for (int i = 0; i < b.nfac; ++i) vals += b.fnnz[i];
+                P.payload_values += vals;
+                if (b.nfac < 1) throw std::runtime_error("butterfly without factors");
+                if (b.fshape[1] != w || b.fshape[2 * (b.nfac - 1)] != h)
+                    throw std::runtime_error("butterfly shape does not match its trim");
+                for (int i = 1; i < b.nfac; ++i)
+                    if (b.fshape[2 * i + 1] != b.fshape[2 * (i - 1)])
+                        throw std::runtime_error("butterfly factor chain shapes mismatch");
+                if (b.nfac == 1) {
+                    // depth 0: a single dense factor (butterfly.py:132-142)
+                    auto d = std::make_unique<std::vector<double>>((size_t)(h * w), 0.0);
+                    for (int64_t e = 0; e < b.fnnz[0]; ++e)
+                        (*d)[b.frows[0][e] * w + b.fcols[0][e]] = b.fvals[0][e];
+                    const double *src = d->data();
+                    keep.push_back(std::move(d));
+                    dense(h_idx, src, w, b.r0, b.r1, b.c0, b.c1);
+                } else {
+                    butterfly(h_idx, b, segs[bi]);
+                }
+            } else {
+                throw std::runtime_error("unknown block kind");
+            }
+        }
+        // group tasks: the last stage of each direction
+        int last = 0;
+        for (int d = 0; d < 2; ++d) last = std::max(last, (int)stages[d].size());
+        for (size_t hi = 0; hi < P.halves.size(); ++hi) {
+            const bf_half &hf = P.halves[hi];
+            if (hf.ncols <= 0) continue;
+            for (size_t g = 0; g < fwd_groups[hi].size(); ++g)
+                add_task(0, last, hf.y + (int32_t)(g * BF_T),
+                         (int32_t)std::min<int64_t>(BF_T, n - (int64_t)g * BF_T),
+                         std::move(fwd_groups[hi][g]));
+            for (size_t g = 0; g < inv_groups[hi].size(); ++g)
+                add_task(1, last, hf.x + (int32_t)(g * BF_T),
+                         (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
+                         std::move(inv_groups[hi][g]));
+        }
+        // flatten: stages in order, tasks by descending cost
+        for (int d = 0; d < 2; ++d) {
+            P.stage_bounds[d].clear();
+            P.stage_bounds[d].push_back((int64_t)P.tasks.size());
+            for (auto &st : stages[d]) {
+                std::stable_sort(st.begin(), st.end(),
+                                 [](const TaskBuild &x, const TaskBuild &y) { return x.cost > y.cost; });
+                for (auto &t : st) {
+                    bf_task tk;
+                    tk.op_begin = (int32_t)P.ops.size();
+                    tk.op_count = (int32_t)t.ops.size();
+                    tk.out = t.out;
+                    tk.nout = t.nout;
+                    P.ops.insert(P.ops.end(), t.ops.begin(), t.ops.end());
+                    if ((int64_t)P.ops.size() > INT32_MAX) throw std::runtime_error("ops exceed int32");
+                    P.tasks.push_back(tk);
+                }
+                P.stage_bounds[d].push_back((int64_t)P.tasks.size());
+            }
+        }
+        // fill tiles
+        const int64_t nj = (int64_t)jobs.size();
+        P.tiles.reset(new double[(size_t)std::max<int64_t>(P.n_tiles, 2)]);
+        double *T = P.tiles.get();
+#pragma omp parallel for schedule(dynamic, 256) num_threads(threads)
+        for (int64_t j = 0; j < nj; ++j) {
+            const TileJob &t = jobs[j];
+            double *dst = T + t.dst;
+            for (int c = 0; c < t.C; ++c)
+                for (int r = 0; r < t.R; ++r)
+                    dst[(int64_t)c * t.R + (r + c) % t.R] = t.src[r * t.rs + c * t.cs];
+            if (((int64_t)t.R * t.C) & 1) dst[(int64_t)t.R * t.C] = 0.0;
+        }
+    }
+};
+
+}  // namespace
+
+extern "C" int bfsht_pack_plan(const bfsht_manifest *man, int threads, bfsht_packed **out) {
+    try {
+        if (!man || !out) throw std::runtime_error("null argument");
+        if (man->n < 1 || man->norders < 0 || man->nblocks < 0) throw std::runtime_error("bad manifest sizes");
+        if (threads <= 0) threads = omp_get_num_procs();
+        auto p = std::make_unique<bfsht_packed>();
+        p->n = man->n;
+        p->norders = man->norders;
+        Packer pk(*p, *man);
+        pk.run(threads);
+        *out = p.release();
+        return 0;
+    } catch (std::exception &e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]) {
+    if (!p) return -1;
+    std::memset(info, 0, 16 * sizeof(int64_t));
+    info[0] = p->n_tiles;
+    info[1] = (int64_t)p->ops.size();
+    info[2] = (int64_t)p->idx.size();
+    info[3] = (int64_t)p->maps.size() / BF_T;
+    info[4] = (int64_t)p->tasks.size();
+    info[5] = p->arena;
+    info[6] = (int64_t)p->halves.size();
+    info[7] = (int64_t)p->stage_bounds[0].size() - 1;
+    info[8] = (int64_t)p->stage_bounds[1].size() - 1;
+    info[9] = p->payload_values;
+    info[10] = p->n_tiles;
+    info[11] = p->n_bf;
+    info[12] = p->n_lr;
+    info[13] = p->n_dn;
+    info[14] = p->n;
+    info[15] = p->norders;
+    return 0;
+}
+
+// arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves,
+//         6 stage bounds fwd (int64, stages+1), 7 stage bounds inv
+extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]) {
+    if (!p) return -1;
+    arrays[0] = p->tiles.get();
+    arrays[1] = p->ops.data();
+    arrays[2] = p->idx.data();
+    arrays[3] = p->maps.data();
+    arrays[4] = p->tasks.data();
+    arrays[5] = p->halves.data();
+    arrays[6] = p->stage_bounds[0].data();
+    arrays[7] = p->stage_bounds[1].data();
+    return 0;
+}
+
+extern "C" void bfsht_packed_free(bfsht_packed *p) { delete p; }

@@ -1,0 +1,516 @@
+// SHT stages around the ALT engine: coefficient packing, the phi-direction
+// DFT of odd length L = 4N-1 fused with parity assembly / quadrature fold,
+// and the per-order ALT boundary kernels.
+//
+// Reference: sht_forward / sht_inverse (pkg/src/bfsht/sht.py:137-166) —
+// per-order alt_forward, phase exp(i m phi0), bin m mod L, L*ifft per
+// colatitude row; and the reverse with fft/L — plus the parity assembly
+// out[n:] = g_e + g_o, out[n-1::-1] = g_e - g_o (alt.py:225-236) and the
+// weighted fold (alt.py:239-253).
+//
+// DFT: in-place mixed-radix decimation-in-time in shared memory, input
+// loaded in digit-reversed order (host-built permutation), twiddles from a
+// host-built exp(-2 pi i k/L) table.  A CTA owns the two rows n+r and
+// n-1-r, so the parity assembly (forward) and the +/- fold (inverse) happen
+// in the same kernel that does the DFT: the ALT node halves are read or
+// written exactly once, as 32-byte sectors.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <algorithm>
+#include <complex>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace {
+
+constexpr int kMaxRadix = 24;
+constexpr int kDftThreads = 512;
+
+struct DftDesc {
+    int L;
+    int nrad;
+    int radix[kMaxRadix];
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 conjif(double2 a, bool c) {
+    return c ? make_double2(a.x, -a.y) : a;
+}
+
+template <int P>
+__device__ __forceinline__ void butterfly(double2 *row, int base, int span, int k, int L,
+                                          const double2 *__restrict__ W, bool inv) {
+    double2 x[P], root[P];
+    const int tstep = L / (span * P);
+    const int rstep = L / P;
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+        x[q] = row[base + q * span];
+        if (q > 0) x[q] = cmul(x[q], conjif(__ldg(W + q * k * tstep), inv));
+        root[q] = conjif(__ldg(W + q * rstep), inv);
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+        double2 acc = x[0];
+#pragma unroll
+        for (int q = 1; q < P; ++q) {
+            double2 t = cmul(x[q], root[(q * s) % P]);
+            acc.x += t.x;
+            acc.y += t.y;
+        }
+        row[base + s * span] = acc;
+    }
+}
+
+// generic radix (large primes), local-memory arrays
+__device__ void butterfly_any(double2 *row, int base, int span, int k, int L, int P,
+                              const double2 *__restrict__ W, bool inv) {
+    double2 x[128];
+    const int tstep = L / (span * P);
+    const int rstep = L / P;
+    for (int q = 0; q < P; ++q) {
+        x[q] = row[base + q * span];
+        if (q > 0) x[q] = cmul(x[q], conjif(__ldg(W + q * k * tstep), inv));
+    }
+    for (int s = 0; s < P; ++s) {
+        double2 acc = x[0];
+        for (int q = 1; q < P; ++q) {
+            double2 t = cmul(x[q], conjif(__ldg(W + ((q * s) % P) * rstep), inv));
+            acc.x += t.x;
+            acc.y += t.y;
+        }
+        row[base + s * span] = acc;
+    }
+}
+
+// All passes over `nrows` rows of buf (row stride L), whole CTA.
+__device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d,
+                           const double2 *__restrict__ W, bool inv) {
+    const int L = d.L;
+    int span = 1;
+    for (int ri = 0; ri < d.nrad; ++ri) {
+        const int P = d.radix[ri];
+        const int nb = L / P;
+        for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
+            const int rw = t / nb, tt = t - rw * nb;
+            const int k = tt % span, g = tt / span;
+            double2 *row = buf + (int64_t)rw * L;
+            const int base = g * span * P + k;
+            switch (P) {
+                case 2: butterfly<2>(row, base, span, k, L, W, inv); break;
+                case 3: butterfly<3>(row, base, span, k, L, W, inv); break;
+                case 4: butterfly<4>(row, base, span, k, L, W, inv); break;
+                case 5: butterfly<5>(row, base, span, k, L, W, inv); break;
+                case 7: butterfly<7>(row, base, span, k, L, W, inv); break;
+                case 11: butterfly<11>(row, base, span, k, L, W, inv); break;
+                case 13: butterfly<13>(row, base, span, k, L, W, inv); break;
+                default: butterfly_any(row, base, span, k, L, P, W, inv); break;
+            }
+        }
+        __syncthreads();
+        span *= P;
+    }
+}
+
+__device__ __forceinline__ double2 *dft_buffer(double2 *scratch, int rows, int L, bool use_smem) {
+    extern __shared__ __align__(16) double2 dsm[];
+    return use_smem ? dsm : scratch + (int64_t)blockIdx.x * rows * L;
+}
+
+// ---- standalone batched DFT: rows of length L (numpy fft / L*ifft)
+__global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
+    DftDesc d, const double2 *__restrict__ in, double2 *__restrict__ out, int64_t rows,
+    const int *__restrict__ perm, const double2 *__restrict__ W, bool inv, bool use_smem,
+    double2 *scratch) {
+    const int L = d.L;
+    double2 *buf = dft_buffer(scratch, 1, L, use_smem);
+    for (int64_t rw = blockIdx.x; rw < rows; rw += gridDim.x) {
+        const double2 *src = in + rw * L;
+        for (int j = threadIdx.x; j < L; j += blockDim.x) buf[perm[j]] = src[j];
+        __syncthreads();
+        dft_passes(buf, 1, d, W, inv);
+        double2 *dst = out + rw * L;
+        for (int j = threadIdx.x; j < L; j += blockDim.x) dst[j] = buf[j];
+        __syncthreads();
+    }
+}
+
+// ---- forward SHT: node halves -> assembled rows -> L*ifft -> grid rows
+__global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
+    DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
+    const double2 *__restrict__ tw, const int *__restrict__ perm,
+    const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
+    double2 *scratch) {
+    const int L = d.L;
+    double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    const int mtop = 2 * n - 1;
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    for (int b = threadIdx.x; b < L; b += blockDim.x) {
+        const int m = b <= mtop ? b : b - L;
+        const int am = m < 0 ? -m : m;
+        const int sel = m < 0 ? 2 : 0;
+        const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
+        double2 go = make_double2(0.0, 0.0), ge = go;
+        if (ho.ncols > 0)
+            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + r) * BF_NRHS + sel);
+        if (he.ncols > 0)
+            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + r) * BF_NRHS + sel);
+        const double2 t = tw[b];
+        const int p = perm[b];
+        buf[p] = cmul(make_double2(ge.x + go.x, ge.y + go.y), t);
+        buf[L + p] = cmul(make_double2(ge.x - go.x, ge.y - go.y), t);
+    }
+    __syncthreads();
+    dft_passes(buf, 2, d, W, true);
+    double2 *up = grid + (int64_t)(n + r) * L;
+    double2 *lo = grid + (int64_t)(n - 1 - r) * L;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        up[j] = buf[j];
+        lo[j] = buf[L + j];
+    }
+    __syncthreads();
+    }
+}
+
+// ---- inverse SHT: grid rows -> fft/L -> phase -> weighted fold -> node halves
+__global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
+    DftDesc d, int n, const bf_half *__restrict__ halves, double *__restrict__ arena,
+    const double2 *__restrict__ tw, const int *__restrict__ perm,
+    const double2 *__restrict__ W, const double2 *__restrict__ grid,
+    const double *__restrict__ weights, bool use_smem, double2 *scratch) {
+    const int L = d.L;
+    double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const double2 *up = grid + (int64_t)(n + r) * L;
+    const double2 *lo = grid + (int64_t)(n - 1 - r) * L;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+        const int p = perm[j];
+        buf[p] = up[j];
+        buf[L + p] = lo[j];
+    }
+    __syncthreads();
+    dft_passes(buf, 2, d, W, false);
+    const double w = weights[n + r];
+    const double invL = 1.0 / (double)L;
+    const int mtop = 2 * n - 1;
+    for (int b = threadIdx.x; b < L; b += blockDim.x) {
+        const int m = b <= mtop ? b : b - L;
+        const int am = m < 0 ? -m : m;
+        const int sel = m < 0 ? 2 : 0;
+        const double2 t = make_double2(tw[b].x, -tw[b].y);
+        double2 sa = buf[b], sb = buf[L + b];
+        sa = cmul(make_double2(sa.x * invL, sa.y * invL), t);
+        sb = cmul(make_double2(sb.x * invL, sb.y * invL), t);
+        const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
+        if (ho.ncols > 0) {
+            double *e = arena + ((int64_t)ho.y + r) * BF_NRHS;
+            *reinterpret_cast<double2 *>(e + sel) =
+                make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
+            if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+        }
+        if (he.ncols > 0) {
+            double *e = arena + ((int64_t)he.y + r) * BF_NRHS;
+            *reinterpret_cast<double2 *>(e + sel) =
+                make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
+            if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+        }
+    }
+    __syncthreads();
+    }
+}
+
+__device__ __forceinline__ int64_t coeff_offset(int m, int K) {
+    // start of order m in ShtCoeffs.pack() (m ascending from -(K-1)), K = 2N
+    if (m <= 0) return (int64_t)(K + m - 1) * (K + m) / 2;
+    return (int64_t)(K - 1) * K / 2 + (int64_t)m * K - (int64_t)m * (m - 1) / 2;
+}
+
+// coefficient halves for the whole SHT: entry = (Re, Im) of +m then -m
+__global__ void coef_pack_kernel(int n, const bf_half *__restrict__ halves,
+                                 const double2 *__restrict__ c, double *__restrict__ arena) {
+    const int am = blockIdx.y;
+    const int K = 2 * n;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * am + par];
+        if (j >= h.ncols) continue;
+        const int k = (par == 0 ? 1 : 0) + 2 * j;
+        const double2 p = c[coeff_offset(am, K) + k];
+        const double2 q = am ? c[coeff_offset(-am, K) + k] : make_double2(0.0, 0.0);
+        double *e = arena + ((int64_t)h.x + j) * BF_NRHS;
+        *reinterpret_cast<double2 *>(e) = p;
+        *reinterpret_cast<double2 *>(e + 2) = q;
+    }
+}
+
+__global__ void coef_unpack_kernel(int n, const bf_half *__restrict__ halves,
+                                   const double *__restrict__ arena, double2 *__restrict__ c) {
+    const int am = blockIdx.y;
+    const int K = 2 * n;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * am + par];
+        if (j >= h.ncols) continue;
+        const int k = (par == 0 ? 1 : 0) + 2 * j;
+        const double *e = arena + ((int64_t)h.x + j) * BF_NRHS;
+        c[coeff_offset(am, K) + k] = *reinterpret_cast<const double2 *>(e);
+        if (am) c[coeff_offset(-am, K) + k] = *reinterpret_cast<const double2 *>(e + 2);
+    }
+}
+
+// ---- per-order boundary (alt_forward / alt_inverse on plans o = 0..)
+// off[o] = start of order o's coefficient vector (length 2N - m_o)
+__global__ void orders_pack_kernel(int n, const bf_half *__restrict__ halves,
+                                   const int64_t *__restrict__ off, const double2 *__restrict__ in,
+                                   double *__restrict__ arena) {
+    const int o = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * o + par];
+        if (j >= h.ncols) continue;
+        const double2 v = in[off[o] + (par == 0 ? 1 : 0) + 2 * j];
+        double *e = arena + ((int64_t)h.x + j) * BF_NRHS;
+        *reinterpret_cast<double2 *>(e) = v;
+        *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+    }
+}
+
+__global__ void orders_unpack_kernel(int n, const bf_half *__restrict__ halves,
+                                     const int64_t *__restrict__ off,
+                                     const double *__restrict__ arena, double2 *__restrict__ out) {
+    const int o = blockIdx.y;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * o + par];
+        if (j >= h.ncols) continue;
+        out[off[o] + (par == 0 ? 1 : 0) + 2 * j] =
+            *reinterpret_cast<const double2 *>(arena + ((int64_t)h.x + j) * BF_NRHS);
+    }
+}
+
+__global__ void orders_assemble_kernel(int n, const bf_half *__restrict__ halves,
+                                       const double *__restrict__ arena, double2 *__restrict__ out) {
+    const int o = blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const bf_half ho = halves[2 * o], he = halves[2 * o + 1];
+    double2 go = make_double2(0.0, 0.0), ge = go;
+    if (ho.ncols > 0) go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + r) * BF_NRHS);
+    if (he.ncols > 0) ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + r) * BF_NRHS);
+    double2 *col = out + (int64_t)o * 2 * n;
+    col[n + r] = make_double2(ge.x + go.x, ge.y + go.y);
+    col[n - 1 - r] = make_double2(ge.x - go.x, ge.y - go.y);
+}
+
+__global__ void orders_fold_kernel(int n, const bf_half *__restrict__ halves,
+                                   const double2 *__restrict__ in, const double *__restrict__ weights,
+                                   double *__restrict__ arena) {
+    const int o = blockIdx.y;
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const double2 *col = in + (int64_t)o * 2 * n;
+    const double2 up = col[n + r], lo = col[n - 1 - r];
+    const double w = weights[n + r];
+    const bf_half ho = halves[2 * o], he = halves[2 * o + 1];
+    if (ho.ncols > 0) {
+        double *e = arena + ((int64_t)ho.y + r) * BF_NRHS;
+        *reinterpret_cast<double2 *>(e) = make_double2(w * (up.x - lo.x), w * (up.y - lo.y));
+        *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+    }
+    if (he.ncols > 0) {
+        double *e = arena + ((int64_t)he.y + r) * BF_NRHS;
+        *reinterpret_cast<double2 *>(e) = make_double2(w * (up.x + lo.x), w * (up.y + lo.y));
+        *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+    }
+}
+
+std::vector<int> factorize(int64_t L) {
+    std::vector<int> f;
+    // prefer the templated radices; 4 only where two 2s pair up
+    for (int p = 2; (int64_t)p * p <= L; ++p)
+        while (L % p == 0) {
+            f.push_back(p);
+            L /= p;
+        }
+    if (L > 1) f.push_back((int)L);
+    return f;
+}
+
+int perm_of(int64_t nidx, const std::vector<int> &rad, int upto) {
+    // position of input index nidx after digit reversal for radices[0..upto)
+    if (upto == 0) return 0;
+    const int p = rad[upto - 1];
+    int64_t M = 1;
+    for (int i = 0; i < upto - 1; ++i) M *= rad[i];
+    return (int)((nidx % p) * M + perm_of(nidx / p, rad, upto - 1));
+}
+
+DftDesc make_desc(const bfsht_plan *pl) {
+    DftDesc d;
+    d.L = (int)pl->dft_L;
+    d.nrad = (int)pl->dft_radix.size();
+    for (int i = 0; i < d.nrad; ++i) d.radix[i] = pl->dft_radix[i];
+    return d;
+}
+
+int dft_smem_bytes(int64_t L, int rows) { return (int)(rows * L * 16); }
+
+}  // namespace
+
+int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
+    if (pl->dft_L == L) return 0;
+    std::vector<int> rad = factorize(L);
+    if ((int)rad.size() > kMaxRadix) {
+        bfsht_set_error("DFT length has too many prime factors");
+        return -4;
+    }
+    for (int p : rad)
+        if (p > 128) {
+            bfsht_set_error("DFT length has a prime factor above 128 (needs Bluestein)");
+            return -4;
+        }
+    std::vector<double> w(2 * L), tw(2 * L);
+    std::vector<int32_t> perm(L);
+    const double two_pi = 6.283185307179586476925286766559;
+    for (int64_t k = 0; k < L; ++k) {
+        // exp(-2 pi i k / L), argument reduced to (-pi, pi] for accuracy
+        int64_t kk = k <= L / 2 ? k : k - L;
+        double a = -two_pi * (double)kk / (double)L;
+        w[2 * k] = std::cos(a);
+        w[2 * k + 1] = std::sin(a);
+        perm[k] = perm_of(k, rad, (int)rad.size());
+    }
+    const int64_t ntop = (L + 1) / 4 * 2 - 1;  // 2N - 1 for L = 4N - 1
+    const double phi0 = 3.14159265358979323846264338327950288 / (double)L;
+    for (int64_t b = 0; b < L; ++b) {
+        int64_t m = b <= ntop ? b : b - L;
+        std::complex<double> t = std::exp(std::complex<double>(0.0, (double)m * phi0));
+        tw[2 * b] = t.real();
+        tw[2 * b + 1] = t.imag();
+    }
+    for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw})
+        if (p) cudaFree(p);
+    BF_CUDA(cudaMalloc(&pl->dft_w, 16 * L));
+    BF_CUDA(cudaMalloc(&pl->dft_tw, 16 * L));
+    BF_CUDA(cudaMalloc(&pl->dft_perm, 4 * L));
+    BF_CUDA(cudaMemcpy(pl->dft_w, w.data(), 16 * L, cudaMemcpyHostToDevice));
+    BF_CUDA(cudaMemcpy(pl->dft_tw, tw.data(), 16 * L, cudaMemcpyHostToDevice));
+    BF_CUDA(cudaMemcpy(pl->dft_perm, perm.data(), 4 * L, cudaMemcpyHostToDevice));
+    pl->dft_radix = rad;
+    pl->dft_L = L;
+    const int need = dft_smem_bytes(L, 2);
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    if (need > maxsm) {
+        const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
+        BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * L * rows));
+        pl->dft_scratch_rows = rows;
+    } else {
+        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+    }
+    return 0;
+}
+
+static int dft_grid_limit(const bfsht_plan *pl) {
+    return pl->dft_scratch ? (int)(pl->dft_scratch_rows / 2) : (1 << 30);
+}
+
+int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStream_t st) {
+    const int n = pl->n;
+    int rc = bf_dft_prepare(pl, 4LL * n - 1);
+    if (rc) return rc;
+    dim3 g1((n + 255) / 256, 2 * n);
+    coef_pack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, reinterpret_cast<const double2 *>(coeffs),
+                                         pl->arena);
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    rc = bf_alt_apply(pl, BFSHT_FORWARD, st);
+    if (rc) return rc;
+    const bool sm = pl->dft_scratch == nullptr;
+    const DftDesc d = make_desc(pl);
+    const int nblk = std::min(n, dft_grid_limit(pl));
+    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+        d, n, pl->halves, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
+        reinterpret_cast<double2 *>(pl->dft_scratch));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const double *weights,
+                   cudaStream_t st) {
+    const int n = pl->n;
+    int rc = bf_dft_prepare(pl, 4LL * n - 1);
+    if (rc) return rc;
+    const bool sm = pl->dft_scratch == nullptr;
+    const DftDesc d = make_desc(pl);
+    const int nblk = std::min(n, dft_grid_limit(pl));
+    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+        d, n, pl->halves, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
+        weights, sm, reinterpret_cast<double2 *>(pl->dft_scratch));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
+    if (rc) return rc;
+    dim3 g1((n + 255) / 256, 2 * n);
+    coef_unpack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, pl->arena,
+                                           reinterpret_cast<double2 *>(coeffs));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+int bf_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out, const double *weights,
+                  cudaStream_t st) {
+    const int n = pl->n, no = pl->norders;
+    if (no == 0) return 0;
+    dim3 g((n + 255) / 256, no);
+    if (dir == BFSHT_FORWARD) {
+        orders_pack_kernel<<<g, 256, 0, st>>>(n, pl->halves, pl->order_off,
+                                              reinterpret_cast<const double2 *>(in), pl->arena);
+        BF_CUDA(cudaGetLastError());
+        int rc = bf_alt_apply(pl, dir, st);
+        if (rc) return rc;
+        orders_assemble_kernel<<<g, 256, 0, st>>>(n, pl->halves, pl->arena,
+                                                  reinterpret_cast<double2 *>(out));
+        BF_CUDA(cudaGetLastError());
+    } else {
+        orders_fold_kernel<<<g, 256, 0, st>>>(n, pl->halves, reinterpret_cast<const double2 *>(in),
+                                              weights, pl->arena);
+        BF_CUDA(cudaGetLastError());
+        int rc = bf_alt_apply(pl, dir, st);
+        if (rc) return rc;
+        orders_unpack_kernel<<<g, 256, 0, st>>>(n, pl->halves, pl->order_off, pl->arena,
+                                                reinterpret_cast<double2 *>(out));
+        BF_CUDA(cudaGetLastError());
+    }
+    pl->launches += 2;
+    return 0;
+}
+
+int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *in, double *out,
+                cudaStream_t st) {
+    int rc = bf_dft_prepare(pl, L);
+    if (rc) return rc;
+    const bool sm = dft_smem_bytes(L, 1) <= 227 * 1024 && pl->dft_scratch == nullptr;
+    int grid = (int)(rows < 4096 ? rows : 4096);
+    if (!sm) grid = (int)std::min<int64_t>(grid, pl->dft_scratch_rows);
+    if (grid <= 0) return 0;
+    dft_rows_kernel<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) : 0, st>>>(
+        make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
+        pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
+        reinterpret_cast<double2 *>(pl->dft_scratch));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}

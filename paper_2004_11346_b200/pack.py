@@ -1,0 +1,201 @@
+"""Reference-layout plans -> packed device format (host side).
+
+``pack_plans(plans)`` flattens a list of ``AltPlan`` objects — from this
+package's planner or from the reference ``bfsht`` itself; only the
+reference attribute names are used (pkg/src/bfsht/alt.py:57-73,
+butterfly.py:45-80, lowrank.py:184-202) — into a ``bfsht_manifest`` and
+calls the native packer (csrc/packer.cpp) through the C ABI.  The result
+is a ``PackedPlan`` holding numpy views of the packed arrays.
+"""
+import ctypes
+
+import numpy as np
+
+from . import native
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+
+class BlockDesc(ctypes.Structure):
+    _fields_ = [("order", _I32), ("parity", _I32), ("kind", _I32),
+                ("r0", _I32), ("r1", _I32), ("c0", _I32), ("c1", _I32),
+                ("rank", _I32), ("a", _P), ("b", _P), ("c", _P),
+                ("nfac", _I32), ("levels", _I32), ("middle", _I32),
+                ("fshape", _P), ("fnnz", _P), ("frows", _P), ("fcols", _P),
+                ("fvals", _P)]
+
+
+class Manifest(ctypes.Structure):
+    _fields_ = [("n", _I32), ("norders", _I32), ("m", _P), ("ncols", _P),
+                ("nblocks", _I64), ("blocks", _P)]
+
+
+def declare(lib):
+    lib.bfsht_pack_plan.restype = ctypes.c_int
+    lib.bfsht_pack_plan.argtypes = [ctypes.POINTER(Manifest), ctypes.c_int,
+                                    ctypes.POINTER(_P)]
+    lib.bfsht_packed_info.restype = ctypes.c_int
+    lib.bfsht_packed_info.argtypes = [_P, ctypes.POINTER(_I64)]
+    lib.bfsht_packed_arrays.restype = ctypes.c_int
+    lib.bfsht_packed_arrays.argtypes = [_P, ctypes.POINTER(_P)]
+    lib.bfsht_packed_free.restype = None
+    lib.bfsht_packed_free.argtypes = [_P]
+    lib.bfsht_host_last_error.restype = ctypes.c_char_p
+    lib.bfsht_host_last_error.argtypes = []
+
+
+OP_DTYPE = np.dtype([("tile", "<i8"), ("in", "<i4"), ("aux", "<i4"),
+                     ("kind", "u1"), ("R", "u1"), ("C", "u1"), ("off", "u1"),
+                     ("flags", "u1"), ("pad0", "u1"), ("pad1", "<u2")])
+TASK_DTYPE = np.dtype([("op_begin", "<i4"), ("op_count", "<i4"),
+                       ("out", "<i4"), ("nout", "<i4")])
+HALF_DTYPE = np.dtype([("x", "<i4"), ("y", "<i4"), ("ncols", "<i4"),
+                       ("m", "<i4")])
+NRHS = 4
+
+INFO_KEYS = ("tile_doubles", "ops", "idx", "maps", "tasks", "arena",
+             "halves", "stages_fwd", "stages_inv", "payload_values",
+             "stored_doubles", "butterfly_blocks", "lowrank_blocks",
+             "dense_blocks", "n", "norders")
+
+
+def _addr(a):
+    return a.ctypes.data if a is not None and a.size else 0
+
+
+class PackedPlan:
+    """Packed device-format plan (host memory, owned by the native packer)."""
+
+    def __init__(self, handle, lib):
+        self._h = handle
+        self._lib = lib
+        info = (_I64 * 16)()
+        lib.bfsht_packed_info(handle, info)
+        self.info = np.array(list(info), dtype=np.int64)
+        self.stats = dict(zip(INFO_KEYS, (int(v) for v in self.info)))
+        arr = (_P * 8)()
+        lib.bfsht_packed_arrays(handle, arr)
+        s = self.stats
+
+        def view(i, dtype, count):
+            if count == 0 or not arr[i]:
+                return np.zeros(0, dtype=dtype)
+            buf = (ctypes.c_char * (count * np.dtype(dtype).itemsize)) \
+                .from_address(arr[i])
+            return np.frombuffer(buf, dtype=dtype, count=count)
+
+        self.tiles = view(0, np.float64, s["tile_doubles"])
+        self.ops = view(1, OP_DTYPE, s["ops"])
+        self.idx = view(2, np.int32, s["idx"])
+        self.maps = view(3, np.int8, s["maps"] * 32)
+        self.tasks = view(4, TASK_DTYPE, s["tasks"])
+        self.halves = view(5, HALF_DTYPE, s["halves"])
+        self.stages_fwd = view(6, np.int64, s["stages_fwd"] + 1)
+        self.stages_inv = view(7, np.int64, s["stages_inv"] + 1)
+
+    @property
+    def n(self):
+        return self.stats["n"]
+
+    @property
+    def orders(self):
+        return self.halves["m"][0::2].copy()
+
+    def payload_bytes(self):
+        """Algorithmic payload bytes read per direction (8 per stored value)."""
+        return 8 * self.stats["payload_values"]
+
+    def close(self):
+        if self._h:
+            self._lib.bfsht_packed_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _kind_of(payload):
+    if hasattr(payload, "factors"):
+        return 0
+    if hasattr(payload, "u") and hasattr(payload, "s"):
+        return 1
+    return 2
+
+
+def pack_plans(plans, n=None, threads=0):
+    """Pack AltPlans (all at the same half-size N) into the device format."""
+    plans = list(plans)
+    if not plans and n is None:
+        raise ValueError("nothing to pack")
+    n = plans[0].n if n is None else n
+    keep = []
+    ms = np.array([p.m for p in plans], dtype=np.int32)
+    ncols = np.zeros(2 * len(plans), dtype=np.int32)
+    descs = []
+    for o, plan in enumerate(plans):
+        if plan.n != n:
+            raise ValueError(f"plan for m={plan.m} has N={plan.n}, expected {n}")
+        for par, (spec, blocks) in enumerate(((plan.spec_odd, plan.blocks_odd),
+                                              (plan.spec_even,
+                                               plan.blocks_even))):
+            if spec is None:
+                continue
+            ncols[2 * o + par] = spec.num_cols
+            for blk in blocks:
+                d = BlockDesc()
+                d.order, d.parity = o, par
+                d.r0, d.r1, d.c0, d.c1 = (int(v) for v in blk.trim)
+                p = blk.payload
+                d.kind = _kind_of(p)
+                if d.kind == 2:
+                    a = np.ascontiguousarray(p, dtype=np.float64)
+                    if a.shape != (d.r1 - d.r0, d.c1 - d.c0):
+                        raise ValueError("dense payload shape does not match "
+                                         "its trim")
+                    keep.append(a)
+                    d.a = _addr(a)
+                elif d.kind == 1:
+                    u = np.ascontiguousarray(p.u, dtype=np.float64)
+                    s = np.ascontiguousarray(p.s, dtype=np.float64)
+                    v = np.ascontiguousarray(p.v, dtype=np.float64)
+                    keep += [u, s, v]
+                    d.rank = s.size
+                    d.a, d.b, d.c = _addr(u), _addr(s), _addr(v)
+                else:
+                    nf = len(p.factors)
+                    shape = np.array([x for f in p.factors for x in f.shape],
+                                     dtype=np.int64)
+                    nnz = np.array([f.vals.size for f in p.factors],
+                                   dtype=np.int64)
+                    rows = [np.ascontiguousarray(f.rows, dtype=np.int64)
+                            for f in p.factors]
+                    cols = [np.ascontiguousarray(f.cols, dtype=np.int64)
+                            for f in p.factors]
+                    vals = [np.ascontiguousarray(f.vals, dtype=np.float64)
+                            for f in p.factors]
+                    rp = (_P * nf)(*[_addr(x) for x in rows])
+                    cp = (_P * nf)(*[_addr(x) for x in cols])
+                    vp = (_P * nf)(*[_addr(x) for x in vals])
+                    keep += [shape, nnz, rows, cols, vals, rp, cp, vp]
+                    d.nfac, d.levels, d.middle = nf, p.levels, p.middle
+                    d.fshape, d.fnnz = _addr(shape), _addr(nnz)
+                    d.frows = ctypes.cast(rp, _P)
+                    d.fcols = ctypes.cast(cp, _P)
+                    d.fvals = ctypes.cast(vp, _P)
+                descs.append(d)
+    arr = (BlockDesc * max(len(descs), 1))(*descs)
+    man = Manifest(n=n, norders=len(plans), m=_addr(ms), ncols=_addr(ncols),
+                   nblocks=len(descs), blocks=ctypes.cast(arr, _P))
+    lib = native.host()
+    out = _P()
+    rc = lib.bfsht_pack_plan(ctypes.byref(man), int(threads), ctypes.byref(out))
+    if rc != 0:
+        raise RuntimeError("bfsht_pack_plan failed: "
+                           + lib.bfsht_host_last_error().decode())
+    del keep
+    return PackedPlan(out, lib)

@@ -21,6 +21,7 @@ from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, replace
 
 import numpy as np
+from threadpoolctl import threadpool_limits
 
 from .factors import (ButterflyFactorization, LowRankFactor,
                       RankOverflowError, SamplingConfig, TableOracle,
@@ -254,7 +255,15 @@ def _empty_stats():
 def plan_alt(n, m, params=None, n0=N0_DEFAULT, tau=TAU_DEFAULT,
              quadrature=None, workers=1):
     """Compressed two-parity plan for order m at half-size n
-    (alt.py:85-152)."""
+    (alt.py:85-152).
+
+    BLAS/LAPACK run single-threaded inside: a threaded reduction could
+    change the last bits of a QR and with them the factors."""
+    with threadpool_limits(limits=1):
+        return _plan_alt(n, m, params, n0, tau, quadrature, workers)
+
+
+def _plan_alt(n, m, params, n0, tau, quadrature, workers):
     if not 0 <= m <= 2 * n - 1:
         raise ValueError(f"order {m} outside [0, {2 * n - 1}]")
     if params is None:

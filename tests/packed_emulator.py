@@ -1,0 +1,101 @@
+"""Numpy interpreter of the packed device format — test infrastructure.
+
+Executes a PackedPlan's stages task by task with the exact semantics the
+CUDA engine implements (csrc/engine.cu, format.h), so the packer can be
+checked against the oracle on CPU, without a GPU.
+"""
+import numpy as np
+
+from paper_2004_11346_b200.pack import NRHS
+
+OP_N, OP_T, OP_ADD = 0, 1, 2
+F_GATHER, F_LANEMAP = 1, 2
+
+
+def tile_matrix(pk, off, R, C):
+    buf = pk.tiles[off:off + R * C]
+    r = np.arange(R)[:, None]
+    c = np.arange(C)[None, :]
+    return buf[c * R + (r + c) % R]
+
+
+def run_direction(pk, arena, direction):
+    bounds = pk.stages_fwd if direction == 0 else pk.stages_inv
+    for s in range(len(bounds) - 1):
+        for t in pk.tasks[bounds[s]:bounds[s + 1]]:
+            acc = np.zeros((32, NRHS))
+            for op in pk.ops[t["op_begin"]:t["op_begin"] + t["op_count"]]:
+                kind, R, C, off = int(op["kind"]), int(op["R"]), int(op["C"]), int(op["off"])
+                gather = bool(op["flags"] & F_GATHER)
+                if kind == OP_ADD:
+                    for j in range(R):
+                        src = int(pk.idx[op["in"] + j]) if gather else int(op["in"]) + j
+                        if src >= 0:
+                            acc[off + j] += arena[src]
+                    continue
+                a = tile_matrix(pk, int(op["tile"]), R, C)
+                nin = C if kind == OP_N else R
+                src = pk.idx[op["in"]:op["in"] + nin] if gather \
+                    else np.arange(op["in"], op["in"] + nin)
+                v = arena[src]
+                res = a @ v if kind == OP_N else a.T @ v
+                width = res.shape[0]
+                for lane in range(32):
+                    if op["flags"] & F_LANEMAP:
+                        sl = int(pk.maps[int(op["aux"]) * 32 + lane])
+                    else:
+                        sl = lane - off
+                    if 0 <= sl < width:
+                        acc[lane] += res[sl]
+            arena[t["out"]:t["out"] + t["nout"]] = acc[:t["nout"]]
+
+
+def alt_orders(pk, plans, direction, vectors, weights=None):
+    """Per-order ALT through the emulated engine: complex vectors in/out."""
+    n = pk.n
+    arena = np.full((pk.stats["arena"], NRHS), np.nan)
+    h = pk.halves
+    outs = []
+    if direction == 0:
+        for o, vec in enumerate(vectors):
+            for par in range(2):
+                hf = h[2 * o + par]
+                if hf["ncols"] == 0:
+                    continue
+                k0 = 1 if par == 0 else 0
+                vals = np.asarray(vec, dtype=np.complex128)[k0::2][:hf["ncols"]]
+                arena[hf["x"]:hf["x"] + hf["ncols"]] = np.stack(
+                    [vals.real, vals.imag, 0 * vals.real, 0 * vals.real], 1)
+        run_direction(pk, arena, 0)
+        for o in range(len(vectors)):
+            go = np.zeros(n, complex)
+            ge = np.zeros(n, complex)
+            for par, g in ((0, go), (1, ge)):
+                hf = h[2 * o + par]
+                if hf["ncols"]:
+                    e = arena[hf["y"]:hf["y"] + n]
+                    g[:] = e[:, 0] + 1j * e[:, 1]
+            col = np.empty(2 * n, complex)
+            col[n:] = ge + go
+            col[n - 1::-1] = ge - go
+            outs.append(col)
+        return outs
+    for o, f in enumerate(vectors):
+        f = np.asarray(f, dtype=np.complex128)
+        up, lo = f[n:], f[n - 1::-1]
+        w = weights[n:]
+        for par, val in ((0, w * (up - lo)), (1, w * (up + lo))):
+            hf = h[2 * o + par]
+            if hf["ncols"]:
+                arena[hf["y"]:hf["y"] + n] = np.stack(
+                    [val.real, val.imag, 0 * val.real, 0 * val.real], 1)
+    run_direction(pk, arena, 1)
+    for o, plan in enumerate(plans):
+        beta = np.zeros(2 * n - plan.m, complex)
+        for par in range(2):
+            hf = h[2 * o + par]
+            if hf["ncols"]:
+                e = arena[hf["x"]:hf["x"] + hf["ncols"]]
+                beta[(1 if par == 0 else 0)::2] = e[:, 0] + 1j * e[:, 1]
+        outs.append(beta)
+    return outs

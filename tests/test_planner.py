@@ -1,0 +1,81 @@
+"""Planner pinned to the reference planner bitwise (golden plan digests)."""
+import numpy as np
+import pytest
+
+from paper_2004_11346_b200 import (SamplingConfig, gauss_legendre, plan_alt,
+                                   plan_sht)
+from paper_2004_11346_b200.plan import make_alt_spec, partition
+
+import golden_data
+from plan_digest import plan_digest
+
+META, ARR = golden_data.load()
+QUADS = {}
+
+
+def _quad(n):
+    if n not in QUADS:
+        QUADS[n] = gauss_legendre(2 * n)
+    return QUADS[n]
+
+
+@pytest.mark.parametrize("case", META["alt"], ids=lambda c: f"n{c['n']}m{c['m']}")
+def test_plan_digest_matches_reference(case):
+    n, m = case["n"], case["m"]
+    plan = plan_alt(n, m, SamplingConfig(tolerance=case["tol"]), n0=case["n0"],
+                    quadrature=_quad(n))
+    assert plan.stats["total_nnz"] == case["total_nnz"]
+    assert plan_digest(plan) == case["digest"]
+
+
+@pytest.mark.parametrize("entry", META["sht"], ids=lambda c: f"n{c['n']}")
+def test_plan_sht_digests(entry):
+    plan = plan_sht(entry["n"])
+    assert [plan_digest(p) for p in plan.alt_plans] == entry["digests"]
+
+
+def test_plan_sht_processes_match_serial():
+    a = plan_sht(16)
+    b = plan_sht(16, processes=3)
+    assert [plan_digest(p) for p in a.alt_plans] == \
+        [plan_digest(p) for p in b.alt_plans]
+    for p in b.alt_plans:
+        assert p.quadrature is b.alt_plans[0].quadrature
+
+
+def test_gauss_legendre_rule():
+    q = gauss_legendre(64)
+    assert np.all(np.diff(q.nodes) > 0)
+    assert abs(q.weights.sum() - 2.0) < 1e-13
+    np.testing.assert_allclose(q.nodes, -q.nodes[::-1], atol=1e-14)
+    for p in (0, 2, 10, 126):
+        exact = 2.0 / (p + 1)
+        assert abs(np.sum(q.weights * q.nodes ** p) - exact) <= 1e-12 * exact
+    q1 = gauss_legendre(1)
+    assert q1.nodes[0] == 0.0 and q1.weights[0] == 2.0
+
+
+def test_plan_validation_and_single_parity():
+    with pytest.raises(ValueError, match="outside"):
+        plan_alt(16, 32, n0=8)
+    with pytest.raises(ValueError, match="outside"):
+        plan_alt(16, -1, n0=8)
+    plan = plan_alt(64, 127, n0=16)
+    assert plan.spec_odd is None and plan.spec_even is not None
+    with pytest.raises(ValueError):
+        plan_sht(0)
+
+
+def test_partition_tiles_half_matrix():
+    spec = make_alt_spec(256, 100, "even", _quad(256))
+    blocks, _ = partition(spec, 64)
+    cover = np.zeros((spec.n, spec.num_cols), dtype=int)
+    for b in blocks:
+        cover[b.row_range[0]:b.row_range[1], b.col_range[0]:b.col_range[1]] += 1
+    assert np.all(cover == 1)
+
+
+def test_threaded_plan_matches_serial():
+    a = plan_alt(128, 128, n0=32, workers=1)
+    b = plan_alt(128, 128, n0=32, workers=4)
+    assert plan_digest(a) == plan_digest(b)
