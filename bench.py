@@ -1,0 +1,423 @@
+#!/usr/bin/env python
+"""Benchmark: SHT forward+inverse transforms/sec (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): full forward then inverse SHT at
+N=1024 — 2048 Gauss-Legendre theta nodes x 4095 phi nodes, complex128
+coefficients beta_{k,m} (k < 2048, |m| <= k) with iid N(0,1) real and
+imaginary parts scaled by (1+k)^-1 (seeded), IDBF tolerance 1e-12, default
+n0 = 512.  A "step" = one sht_forward + one sht_inverse over that input.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value`: transforms/sec with plan and data resident in HBM (device-timed
+with CUDA events, max over ranks).  `e2e`: the same metric through the
+public host API (coefficients in host memory -> grid on host -> back),
+host<->device copies inside the timed region.  The payload (13.5 GB of fp64
+factor values at N=1024) is far larger than the 126 MB L2, so every step
+streams it from HBM (no flush needed; stated in `config`).
+
+Multi-GPU (torchrun, one rank per GPU): orders |m| are sharded by LPT on
+payload bytes; each rank applies its orders' ALT, and one NCCL all-to-all
+per direction moves g(m, theta) between the m-major ALT stage and the
+theta-major DFT stage (paper_2004_11346_b200/dist.py).  Total work is fixed
+as N grows ("strong" scaling).
+
+`--impl reference`: the reference's own CPU algorithm (the oracle port,
+oracle/apply.py, which reproduces the reference outputs bitwise) on all host
+cores of rank 0: orders are dealt to one process per core, numpy FFT in the
+parent.  Same metric/config; other ranks exit without work.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sht_fwd_inv_transforms_per_sec"
+UNIT = "transforms/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1024)
+    ap.add_argument("--tol", type=float, default=1e-12)
+    ap.add_argument("--plan-procs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--check", action="store_true",
+                    help="verify GPU output against the CPU oracle")
+    return ap.parse_args()
+
+
+def synthetic_coeffs(n, seed=0):
+    """(1+k)^-1-scaled iid N(0,1) complex coefficients, ShtCoeffs.pack()
+    order (m ascending from -(2N-1), real part block then imaginary)."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for m in range(-(2 * n - 1), 2 * n):
+        ln = 2 * n - abs(m)
+        k = np.arange(abs(m), 2 * n, dtype=np.float64)
+        re = rng.standard_normal(ln)
+        im = rng.standard_normal(ln)
+        parts.append((re + 1j * im) / (1.0 + k))
+    return np.concatenate(parts)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for name, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------- reference arm
+_REF_STATE = {}
+
+
+def _ref_worker_init(n, orders, tol):
+    from paper_2004_11346_b200 import SamplingConfig, plan_orders
+    os.environ["OMP_NUM_THREADS"] = "1"
+    plans = plan_orders(n, orders, SamplingConfig(tolerance=tol), processes=1)
+    _REF_STATE["plans"] = {p.m: p for p in plans}
+
+
+def _ref_worker_forward(job):
+    import oracle.apply as OA
+    from threadpoolctl import threadpool_limits
+    out = {}
+    with threadpool_limits(limits=1):
+        for m, vec in job:
+            out[m] = OA.alt_forward(_REF_STATE["plans"][abs(m)], vec)
+    return out
+
+
+def _ref_worker_inverse(job):
+    import oracle.apply as OA
+    from threadpoolctl import threadpool_limits
+    out = {}
+    with threadpool_limits(limits=1):
+        for m, col in job:
+            out[m] = OA.alt_inverse(_REF_STATE["plans"][abs(m)], col)
+    return out
+
+
+def _ref_worker_ready(_):
+    return len(_REF_STATE.get("plans", {}))
+
+
+def run_reference(args):
+    """CPU arm: the reference algorithm (oracle port) on every host core."""
+    import multiprocessing as mp
+    import oracle.apply as OA
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    n = args.n
+    cores = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    # every core plans and owns a round-robin share of |m|
+    shards = [list(range(r, 2 * n, cores)) for r in range(cores)]
+    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(n, s, args.tol))
+             for s in shards]
+    t0 = time.time()
+    for p in pools:
+        p.apply(_ref_worker_ready, (0,))
+    t_plan = time.time() - t0
+    flat = synthetic_coeffs(n)
+    ms, offs = OA.coeff_offsets(n)
+    num_phi, _, bins = OA.bins(n)
+    phi0 = np.pi / num_phi
+
+    def step():
+        jobs = [[] for _ in shards]
+        for i, m in enumerate(ms):
+            jobs[abs(m) % cores].append((int(m), flat[offs[i]:offs[i + 1]]))
+        res = [p.apply_async(_ref_worker_forward, (j,)) for p, j in zip(pools, jobs)]
+        buf = np.zeros((2 * n, num_phi), dtype=np.complex128)
+        for r in res:
+            for m, g in r.get().items():
+                buf[:, m % num_phi] = g * np.exp(1j * m * phi0)
+        grid = num_phi * np.fft.ifft(buf, axis=1)
+        spectrum = np.fft.fft(grid, axis=1) / num_phi
+        jobs = [[] for _ in shards]
+        for m in ms:
+            g = spectrum[:, m % num_phi] * np.exp(-1j * m * phi0)
+            jobs[abs(m) % cores].append((int(m), g))
+        res = [p.apply_async(_ref_worker_inverse, (j,)) for p, j in zip(pools, jobs)]
+        out = np.zeros(offs[-1], dtype=np.complex128)
+        for r in res:
+            for m, b in r.get().items():
+                i = m + 2 * n - 1
+                out[offs[i]:offs[i + 1]] = b
+        return out
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    for p in pools:
+        p.terminate()
+    value = args.steps / dt
+    sample = (f"full N={n} SHT fwd+inv per step, {cores} processes "
+              f"(one per host core, orders dealt round-robin, numpy FFT in "
+              f"parent); planning {t_plan:.1f}s excluded")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C2: SHT fwd+inv N={n}, tol {args.tol:g}",
+                   "n": n, "tol": args.tol, "n0": 512},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+def cpu_baseline_single(plans, n, flat):
+    """Oracle (reference algorithm) on one host core: one full fwd+inv."""
+    import oracle.apply as OA
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        grid = OA.sht_forward(plans, n, flat)
+        t1 = time.perf_counter()
+        OA.sht_inverse(plans, n, grid)
+        t2 = time.perf_counter()
+    return 1.0 / (t2 - t0), {"fwd_s": t1 - t0, "inv_s": t2 - t1}, grid
+
+
+def run_ours(args):
+    import torch
+    from paper_2004_11346_b200 import SamplingConfig, plan_orders
+    from paper_2004_11346_b200.api import ShtDevice, DevicePlan
+    from paper_2004_11346_b200 import dist as D
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.n
+    params = SamplingConfig(tolerance=args.tol)
+    procs = args.plan_procs or max(1, (os.cpu_count() or 1) // world)
+
+    t0 = time.time()
+    if world == 1:
+        orders = list(range(2 * n))
+    else:
+        orders = D.lpt_orders(n, world)[rank]
+    plans = plan_orders(n, orders, params, processes=procs)
+    t_plan = time.time() - t0
+    payload_values = sum(p.stats["total_nnz"] for p in plans)
+
+    t0 = time.time()
+    if world == 1:
+        eng = ShtDevice.__new__(ShtDevice)
+        eng.n = n
+        eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights)
+        runner = D.SingleRunner(eng)
+    else:
+        runner = D.ShardedSht(n, plans, orders, rank, world)
+    torch.cuda.synchronize()
+    t_up = time.time() - t0
+
+    flat = synthetic_coeffs(n)
+    dev = torch.device("cuda", local)
+    coeffs, grid, back = runner.make_buffers(flat)
+
+    def step():
+        runner.forward(coeffs, grid)
+        runner.inverse(grid, back)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # -------------------------------------------------- timed: device-resident
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = runner.launches_total()
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    barrier()
+    launches = runner.launches_total() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    clk = clocks.stop()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = 1e3 / ms
+
+    # ------------------------------------- roofline: ALT stage, device events
+    alt = runner.time_alt(reps=3)
+    if world > 1:
+        t = torch.tensor([alt["fwd_ms"], alt["inv_ms"]], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        alt["fwd_ms"], alt["inv_ms"] = (float(v) for v in t.tolist())
+    alt_bytes = runner.alt_bytes()          # per direction, this rank
+    if world > 1:
+        t = torch.tensor([float(alt_bytes)], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        alt_bytes_all = float(t.item())
+    else:
+        alt_bytes_all = float(alt_bytes)
+    peak, peak_kind = measured_peaks()
+    alt_ms = 0.5 * (alt["fwd_ms"] + alt["inv_ms"])
+    achieved = alt_bytes_all / world / (alt_ms * 1e-3) / 1e9  # per GPU
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "kernel": "alt_stage_kernel (all ALT stages of one direction)",
+                "alt_fwd_ms": alt["fwd_ms"], "alt_inv_ms": alt["inv_ms"],
+                "alg_bytes_per_direction": alt_bytes_all / world,
+                "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
+
+    # ------------------------------------------------ e2e via the host API
+    e2e = runner.time_e2e(flat, args.steps, args.warmup, barrier)
+    if world > 1:
+        t = torch.tensor([e2e["ms"]], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e["ms"] = float(t.item())
+
+    check = None
+    if args.check and world == 1:
+        import oracle.apply as OA
+        g = grid.cpu().numpy()
+        want = OA.sht_forward(plans, n, flat)
+        check = float(np.linalg.norm(g - want) / np.linalg.norm(want))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, detail, _ = cpu_baseline_single(plans, n, flat)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"one full N={n} SHT fwd+inv with the oracle port of "
+                         f"the reference apply (fwd {detail['fwd_s']:.1f}s, "
+                         f"inv {detail['inv_s']:.1f}s), 1 core, BLAS threads 1"}
+
+    rt = runner.roundtrip_error(coeffs, grid, back)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C2: SHT fwd+inv N={n}, tol {args.tol:g}",
+                       "n": n, "tol": args.tol, "n0": 512,
+                       "grid": [2 * n, 4 * n - 1],
+                       "payload_values_rank0": int(payload_values),
+                       "l2": "inputs larger than L2 (13.5 GB payload streamed per direction)",
+                       "parallelism": f"orders sharded over {world} GPU(s)"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": {"value": 1e3 / e2e["ms"], "unit": UNIT,
+                    "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "roundtrip_rel_l2": rt,
+            "setup_s": {"plan": t_plan, "pack_upload": t_up},
+        }
+        if check is not None:
+            line["check_rel_l2_vs_oracle"] = check
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -127,8 +127,34 @@ int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
 int bfsht_dft_rows(int64_t L, int64_t rows, int dir, const double *in,
                    double *out, void *stream);
 
-/* Number of kernel launches issued by the last apply on this plan. */
+/* Kernel launches issued on this plan since creation or the last reset. */
 int64_t bfsht_plan_launches(bfsht_plan *pl);
+int bfsht_reset_launches(bfsht_plan *pl);
+
+/* ----------------------------------------- multi-GPU (order-sharded) SHT
+ * A rank's plan holds its share of the orders.  Coefficient shard layout:
+ * per plan order o, the +m vector at off[o] (2N-m values, k ascending) and,
+ * for m > 0, the -m vector right after it.  Node-half entries are moved
+ * between ranks with gather/scatter (4 doubles per entry, index lists into
+ * the arena) around an NCCL all-to-all; the DFT stage then works on the
+ * rank's row pairs r in [r_begin, r_begin + r_count): `halves` (device,
+ * bf_half per (order, parity) for ALL 2N orders) locates each order's
+ * entries in `ybuf` at .y + (r - r_begin); the local grid holds rows
+ * n-r_begin-r_count .. n-r_begin-1 then n+r_begin .. n+r_begin+r_count-1. */
+int bfsht_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs,
+                     void *stream);
+int bfsht_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs,
+                       void *stream);
+int bfsht_gather_entries(bfsht_plan *pl, const int32_t *idx, int64_t count,
+                         double *out, void *stream);
+int bfsht_scatter_entries(bfsht_plan *pl, const int32_t *idx, int64_t count,
+                          const double *in, void *stream);
+int bfsht_synth_rows(bfsht_plan *pl, const void *halves, const double *ybuf,
+                     int64_t r_begin, int64_t r_count, double *grid,
+                     void *stream);
+int bfsht_anal_rows(bfsht_plan *pl, const void *halves, double *ubuf,
+                    int64_t r_begin, int64_t r_count, const double *grid,
+                    const double *weights, void *stream);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,8 @@ from .factors import (ButterflyFactorization, LowRankFactor, RankOverflowError,
                       SamplingConfig, SparseFactor, idbf_factor)
 from .legendre import QuadratureRule, gauss_legendre, legendre_table
 from .plan import (N0_DEFAULT, TAU_DEFAULT, AltPlan, Block, ShtPlan,
-                   make_alt_spec, plan_alt, plan_diagnostics, plan_sht)
+                   make_alt_spec, plan_alt, plan_diagnostics, plan_orders,
+                   plan_sht)
 from .sht import ShtCoeffs, ShtGrid, ShtGridValues, make_grid
 
 __all__ = [
@@ -18,7 +19,7 @@ __all__ = [
     "SamplingConfig", "SparseFactor", "idbf_factor", "QuadratureRule",
     "gauss_legendre", "legendre_table", "N0_DEFAULT", "TAU_DEFAULT",
     "AltPlan", "Block", "ShtPlan", "make_alt_spec", "plan_alt",
-    "plan_diagnostics", "plan_sht", "ShtCoeffs", "ShtGrid", "ShtGridValues",
+    "plan_diagnostics", "plan_orders", "plan_sht", "ShtCoeffs", "ShtGrid", "ShtGridValues",
     "make_grid", "alt_forward", "alt_inverse", "sht_forward", "sht_inverse",
     "CoeffVector", "GridFunctionColumn", "DevicePlan", "ShtDevice",
 ]

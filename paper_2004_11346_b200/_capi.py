@@ -33,6 +33,18 @@ def declare(lib):
     lib.bfsht_sht_inverse.argtypes = [_P, _P, _P, _P, _P]
     lib.bfsht_dft_rows.restype = _I
     lib.bfsht_dft_rows.argtypes = [_I64, _I64, _I, _P, _P, _P]
+    lib.bfsht_reset_launches.restype = _I
+    lib.bfsht_reset_launches.argtypes = [_P]
+    for name in ("bfsht_shard_pack", "bfsht_shard_unpack"):
+        getattr(lib, name).restype = _I
+        getattr(lib, name).argtypes = [_P, _P, _P, _P]
+    for name in ("bfsht_gather_entries", "bfsht_scatter_entries"):
+        getattr(lib, name).restype = _I
+        getattr(lib, name).argtypes = [_P, _P, _I64, _P, _P]
+    lib.bfsht_synth_rows.restype = _I
+    lib.bfsht_synth_rows.argtypes = [_P, _P, _P, _I64, _I64, _P, _P]
+    lib.bfsht_anal_rows.restype = _I
+    lib.bfsht_anal_rows.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
 
 
 # every symbol include/bfsht_b200.h declares (checked by tests on CPU)
@@ -42,6 +54,9 @@ EXPORTS = (
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
     "bfsht_alt_apply", "bfsht_alt_orders", "bfsht_sht_forward",
     "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
+    "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",
+    "bfsht_gather_entries", "bfsht_scatter_entries", "bfsht_synth_rows",
+    "bfsht_anal_rows",
 )
 
 

@@ -152,7 +152,7 @@ int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream) {
         g_err = "bad plan or direction";
         return -1;
     }
-    pl->launches = 0;
+
     return bf_alt_apply(pl, dir, (cudaStream_t)stream);
 }
 
@@ -166,7 +166,7 @@ int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
         g_err = "inverse ALT needs quadrature weights";
         return -1;
     }
-    pl->launches = 0;
+
     return bf_alt_orders(pl, dir, in, out, weights, (cudaStream_t)stream);
 }
 
@@ -189,7 +189,7 @@ static int check_sht(bfsht_plan *pl) {
 
 int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, void *stream) {
     if (check_sht(pl)) return -1;
-    pl->launches = 0;
+
     return bf_sht_forward(pl, coeffs, grid, (cudaStream_t)stream);
 }
 
@@ -200,7 +200,7 @@ int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
         g_err = "inverse SHT needs quadrature weights";
         return -1;
     }
-    pl->launches = 0;
+
     return bf_sht_inverse(pl, grid, coeffs, weights, (cudaStream_t)stream);
 }
 

@@ -144,13 +144,18 @@ __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
 // ---- forward SHT: node halves -> assembled rows -> L*ifft -> grid rows
 __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
-    const double2 *__restrict__ tw, const int *__restrict__ perm,
+    int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
     double2 *scratch) {
+    // node-half entries of row pair r live at halves[.].y + (r - r_begin);
+    // grid holds 2*r_count local rows: lower rows n-r_begin-r_count .. n-r_begin-1
+    // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
+    // r_begin = 0, r_count = n)
     const int L = d.L;
     double2 *buf = dft_buffer(scratch, 2, L, use_smem);
     const int mtop = 2 * n - 1;
-    for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
+    const int rr = r - r_begin;
     for (int b = threadIdx.x; b < L; b += blockDim.x) {
         const int m = b <= mtop ? b : b - L;
         const int am = m < 0 ? -m : m;
@@ -158,9 +163,9 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
         double2 go = make_double2(0.0, 0.0), ge = go;
         if (ho.ncols > 0)
-            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + r) * BF_NRHS + sel);
+            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + rr) * BF_NRHS + sel);
         if (he.ncols > 0)
-            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + r) * BF_NRHS + sel);
+            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + rr) * BF_NRHS + sel);
         const double2 t = tw[b];
         const int p = perm[b];
         buf[p] = cmul(make_double2(ge.x + go.x, ge.y + go.y), t);
@@ -168,8 +173,8 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     }
     __syncthreads();
     dft_passes(buf, 2, d, W, true);
-    double2 *up = grid + (int64_t)(n + r) * L;
-    double2 *lo = grid + (int64_t)(n - 1 - r) * L;
+    double2 *up = grid + (int64_t)(r_count + rr) * L;
+    double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         up[j] = buf[j];
         lo[j] = buf[L + j];
@@ -183,12 +188,14 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, double *__restrict__ arena,
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
-    const double *__restrict__ weights, bool use_smem, double2 *scratch) {
+    const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
+    double2 *scratch) {
     const int L = d.L;
     double2 *buf = dft_buffer(scratch, 2, L, use_smem);
-    for (int r = blockIdx.x; r < n; r += gridDim.x) {
-    const double2 *up = grid + (int64_t)(n + r) * L;
-    const double2 *lo = grid + (int64_t)(n - 1 - r) * L;
+    for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
+    const int rr = r - r_begin;
+    const double2 *up = grid + (int64_t)(r_count + rr) * L;
+    const double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         const int p = perm[j];
         buf[p] = up[j];
@@ -209,13 +216,13 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
         sb = cmul(make_double2(sb.x * invL, sb.y * invL), t);
         const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
         if (ho.ncols > 0) {
-            double *e = arena + ((int64_t)ho.y + r) * BF_NRHS;
+            double *e = arena + ((int64_t)ho.y + rr) * BF_NRHS;
             *reinterpret_cast<double2 *>(e + sel) =
                 make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
             if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
         }
         if (he.ncols > 0) {
-            double *e = arena + ((int64_t)he.y + r) * BF_NRHS;
+            double *e = arena + ((int64_t)he.y + rr) * BF_NRHS;
             *reinterpret_cast<double2 *>(e + sel) =
                 make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
             if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
@@ -438,7 +445,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
     sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
-        d, n, pl->halves, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        d, n, pl->halves, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
@@ -457,7 +464,7 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
         d, n, pl->halves, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, sm, reinterpret_cast<double2 *>(pl->dft_scratch));
+        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
@@ -509,6 +516,42 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
     dft_rows_kernel<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) : 0, st>>>(
         make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
+        reinterpret_cast<double2 *>(pl->dft_scratch));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int r_begin,
+                  int r_count, double *grid, cudaStream_t st) {
+    const int n = pl->n;
+    int rc = bf_dft_prepare(pl, 4LL * n - 1);
+    if (rc) return rc;
+    if (r_count <= 0) return 0;
+    const bool sm = pl->dft_scratch == nullptr;
+    const int nblk = std::min(r_count, dft_grid_limit(pl));
+    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+        make_desc(pl), n, halves, ybuf, r_begin, r_count,
+        reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
+        reinterpret_cast<double2 *>(pl->dft_scratch));
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begin, int r_count,
+                 const double *grid, const double *weights, cudaStream_t st) {
+    const int n = pl->n;
+    int rc = bf_dft_prepare(pl, 4LL * n - 1);
+    if (rc) return rc;
+    if (r_count <= 0) return 0;
+    const bool sm = pl->dft_scratch == nullptr;
+    const int nblk = std::min(r_count, dft_grid_limit(pl));
+    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+        make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
+        pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
+        reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;

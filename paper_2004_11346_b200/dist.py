@@ -1,0 +1,334 @@
+"""SHT runners: one GPU, or orders sharded over the GPUs of one node.
+
+Sharding: the independent unit is the order |m| — its plan
+serves +m and -m (pkg/src/bfsht/sht.py:146,165) — so each rank plans,
+packs and applies the ALT for its own orders only (greedy LPT on the
+per-order cost proxy 2N-|m|).  The phi DFT needs every order of a
+colatitude row (sht.py:148,161), so each direction has exactly one exchange:
+an NCCL all-to-all that transposes node-half entries between the m-major
+ALT layout (owner of m) and the theta-major DFT layout (owner of row pairs
+r, n+r / n-1-r).  Entries are moved with gather/scatter kernels into
+contiguous per-destination chunks, so the collective is a single
+``all_to_all_single`` per direction.
+
+Both runners expose the same interface to bench.py / smoke():
+forward(coeffs, grid), inverse(grid, coeffs), time_alt, time_e2e, ...
+"""
+import ctypes
+
+import numpy as np
+
+from ._capi import check
+from .pack import HALF_DTYPE, NRHS
+
+FORWARD, INVERSE = 0, 1
+
+
+def lpt_orders(n, world):
+    """Greedy LPT assignment of orders 0..2N-1 to ``world`` ranks on the
+    proxy cost 2N - m (corr. 0.99 with payload bytes)."""
+    loads = [0.0] * world
+    out = [[] for _ in range(world)]
+    for m in range(2 * n):  # descending cost order
+        r = min(range(world), key=lambda i: (loads[i], i))
+        out[r].append(m)
+        loads[r] += 2 * n - m
+    return [sorted(o) for o in out]
+
+
+def row_split(n, world):
+    """Row pairs r in [0, n) split into contiguous near-equal ranges."""
+    return [(q * n // world, (q + 1) * n // world) for q in range(world)]
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(torch):
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _Common:
+    def launches_total(self):
+        return int(self.dp.lib.bfsht_plan_launches(self.dp.handle))
+
+    def alt_bytes(self):
+        """Algorithmic ALT bytes per direction on this rank: every stored
+        payload value once (8 B) + coefficient-half and node-half entries
+        once (4 x 8 B each)."""
+        h = self.dp.packed.halves
+        present = h["ncols"] > 0
+        entries = int(h["ncols"][present].sum()) + int(present.sum()) * self.n
+        return 8 * self.dp.packed.stats["payload_values"] + 32 * entries
+
+    def time_alt(self, reps=3):
+        import torch
+        out = {}
+        for name, d in (("fwd_ms", FORWARD), ("inv_ms", INVERSE)):
+            self.dp.alt_apply(d)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                self.dp.alt_apply(d)
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = e0.elapsed_time(e1) / reps
+        return out
+
+
+class SingleRunner(_Common):
+    """Whole SHT on one GPU (plan holds every order)."""
+
+    def __init__(self, sht_device):
+        self.dev = sht_device
+        self.dp = sht_device.plan
+        self.n = sht_device.n
+        self._pinned = None
+
+    def make_buffers(self, flat):
+        import torch
+        dev = self.dp.device
+        n = self.n
+        c = torch.from_numpy(np.ascontiguousarray(flat)).to(dev)
+        g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128, device=dev)
+        return c, g, torch.empty_like(c)
+
+    def forward(self, coeffs, grid):
+        self.dp.sht_forward(coeffs, grid)
+
+    def inverse(self, grid, coeffs):
+        self.dp.sht_inverse(grid, coeffs)
+
+    def roundtrip_error(self, coeffs, grid, back):
+        self.forward(coeffs, grid)
+        self.inverse(grid, back)
+        import torch
+        return float(torch.linalg.norm(back - coeffs) / torch.linalg.norm(coeffs))
+
+    def time_e2e(self, flat, steps, warmup, barrier):
+        """Host API: numpy coefficients -> host grid -> host coefficients,
+        copies through pinned buffers inside the timed region."""
+        import torch
+        dev = self.dp.device
+        n = self.n
+        h_c = torch.from_numpy(flat).pin_memory()
+        h_g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128).pin_memory()
+        h_b = torch.empty_like(h_c).pin_memory()
+        d_c = torch.empty(h_c.shape, dtype=torch.complex128, device=dev)
+        d_g = torch.empty(h_g.shape, dtype=torch.complex128, device=dev)
+        d_b = torch.empty_like(d_c)
+
+        def step():
+            d_c.copy_(h_c, non_blocking=True)
+            self.dp.sht_forward(d_c, d_g)
+            h_g.copy_(d_g, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # grid is on the host
+            d_g.copy_(h_g, non_blocking=True)
+            self.dp.sht_inverse(d_g, d_b)
+            h_b.copy_(d_b, non_blocking=True)
+            torch.cuda.current_stream().synchronize()   # coefficients on host
+
+        for _ in range(warmup):
+            step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        barrier()
+        nb_c = h_c.numel() * 16
+        nb_g = h_g.numel() * 16
+        return {"ms": e0.elapsed_time(e1) / steps, "h2d": nb_c + nb_g,
+                "d2h": nb_g + nb_c}
+
+
+class ShardedSht(_Common):
+    """Orders sharded over ranks, one NCCL all-to-all per direction.
+
+    Data layout per rank: coefficients of its own orders (shard layout, see
+    bfsht_shard_pack), and grid rows of its row pairs
+    [r0, r1): rows n-r1..n-r0-1 then n+r0..n+r1-1.
+    """
+
+    def __init__(self, n, plans, orders, rank, world, group=None):
+        import torch
+        import torch.distributed as dist
+        from .api import DevicePlan
+        self.torch, self.dist = torch, dist
+        self.n, self.rank, self.world = n, rank, world
+        self.group = group
+        self.orders = list(orders)
+        self.dp = DevicePlan(plans, weights=plans[0].quadrature.weights
+                             if plans else None)
+        lib = self.dp.lib
+        self.lib = lib
+        dev = self.dp.device
+        # every rank's order list (deterministic, no communication needed)
+        self.all_orders = lpt_orders(n, world)
+        assert self.all_orders[rank] == self.orders, "orders must follow lpt_orders"
+        self.rows = row_split(n, world)
+        r0, r1 = self.rows[rank]
+        self.r0, self.rc = r0, r1 - r0
+        # presence of each (order, parity) half: needs only N and m
+        def ncols(m, par):
+            half = (m + 1) // 2 if par == 0 else m // 2
+            return max(n - half, 0)
+
+        # --- send side: entries of my orders' node halves, by destination
+        h = self.dp.packed.halves
+        send_idx, send_counts = [], []
+        for q in range(world):
+            a, b = self.rows[q]
+            cnt = 0
+            for o in range(len(self.orders)):
+                for par in range(2):
+                    hf = h[2 * o + par]
+                    if hf["ncols"] == 0:
+                        continue
+                    send_idx.append(np.arange(hf["y"] + a, hf["y"] + b, dtype=np.int32))
+                    cnt += b - a
+            send_counts.append(cnt)
+        self.send_idx = torch.from_numpy(np.concatenate(send_idx) if send_idx
+                                         else np.zeros(0, np.int32)).to(dev)
+        self.send_counts = send_counts
+        # --- receive side: my row pairs for every order, chunked by source
+        recv_halves = np.zeros(4 * n, dtype=HALF_DTYPE)
+        recv_counts = []
+        pos = 0
+        for s in range(world):
+            cnt = 0
+            for m in self.all_orders[s]:
+                for par in range(2):
+                    recv_halves[2 * m + par]["m"] = m
+                    nc = ncols(m, par)
+                    recv_halves[2 * m + par]["ncols"] = nc
+                    if nc == 0:
+                        continue
+                    recv_halves[2 * m + par]["y"] = pos
+                    pos += self.rc
+                    cnt += self.rc
+            recv_counts.append(cnt)
+        self.recv_counts = recv_counts
+        self.recv_entries = pos
+        self.recv_halves = torch.from_numpy(recv_halves.view(np.int32).copy()).to(dev)
+        self.sendbuf = torch.zeros((max(sum(send_counts), 1), NRHS), dtype=torch.float64, device=dev)
+        self.recvbuf = torch.zeros((max(pos, 1), NRHS), dtype=torch.float64, device=dev)
+        # coefficient shard offsets: +m then -m per local order
+        offs, at = [], 0
+        for m in self.orders:
+            offs.append(at)
+            at += (2 * n - m) * (2 if m else 1)
+        self.coeff_len = at
+        self.coeff_off = torch.tensor(offs + [at], dtype=torch.int64, device=dev)
+        self.weights = self.dp.weights
+
+    def make_buffers(self, flat):
+        torch = self.torch
+        dev = self.dp.device
+        c = torch.from_numpy(self.shard_coeffs(flat)).to(dev)
+        g = torch.empty((2 * self.rc, 4 * self.n - 1), dtype=torch.complex128, device=dev)
+        return c, g, torch.empty_like(c)
+
+    # --------------------------------------------------------- transforms
+    def _a2a(self, out, inp, out_counts, in_counts):
+        self.dist.all_to_all_single(out.view(-1), inp.view(-1),
+                                    [c * NRHS for c in out_counts],
+                                    [c * NRHS for c in in_counts], group=self.group)
+
+    def forward(self, coeffs, grid):
+        lib, dp, st = self.lib, self.dp, _stream(self.torch)
+        check(lib, lib.bfsht_shard_pack(dp.handle, _ptr(self.coeff_off), _ptr(coeffs), st),
+              "bfsht_shard_pack")
+        dp.alt_apply(FORWARD)
+        check(lib, lib.bfsht_gather_entries(dp.handle, _ptr(self.send_idx),
+                                            self.send_idx.numel(), _ptr(self.sendbuf), st),
+              "bfsht_gather_entries")
+        self._a2a(self.recvbuf, self.sendbuf, self.recv_counts, self.send_counts)
+        check(lib, lib.bfsht_synth_rows(dp.handle, _ptr(self.recv_halves), _ptr(self.recvbuf),
+                                        self.r0, self.rc, _ptr(grid), st), "bfsht_synth_rows")
+
+    def inverse(self, grid, coeffs):
+        lib, dp, st = self.lib, self.dp, _stream(self.torch)
+        check(lib, lib.bfsht_anal_rows(dp.handle, _ptr(self.recv_halves), _ptr(self.recvbuf),
+                                       self.r0, self.rc, _ptr(grid), _ptr(self.weights), st),
+              "bfsht_anal_rows")
+        self._a2a(self.sendbuf, self.recvbuf, self.send_counts, self.recv_counts)
+        check(lib, lib.bfsht_scatter_entries(dp.handle, _ptr(self.send_idx),
+                                             self.send_idx.numel(), _ptr(self.sendbuf), st),
+              "bfsht_scatter_entries")
+        dp.alt_apply(INVERSE)
+        check(lib, lib.bfsht_shard_unpack(dp.handle, _ptr(self.coeff_off), _ptr(coeffs), st),
+              "bfsht_shard_unpack")
+
+    def shard_coeffs(self, flat):
+        """This rank's coefficient shard from the full flat layout."""
+        n = self.n
+        parts = []
+        for m in self.orders:
+            for mm in ((m, -m) if m else (m,)):
+                start = _flat_offset(n, mm)
+                parts.append(flat[start:start + 2 * n - abs(mm)])
+        return np.concatenate(parts)
+
+    def shard_grid(self, full):
+        n = self.n
+        r0, r1 = self.r0, self.r0 + self.rc
+        return np.concatenate([full[n - r1:n - r0], full[n + r0:n + r1]])
+
+    def roundtrip_error(self, coeffs, grid, back):
+        torch = self.torch
+        self.forward(coeffs, grid)
+        self.inverse(grid, back)
+        num = torch.linalg.norm(back - coeffs) ** 2
+        den = torch.linalg.norm(coeffs) ** 2
+        t = torch.stack([num, den])
+        self.dist.all_reduce(t, group=self.group)
+        return float((t[0] / t[1]).sqrt())
+
+    def time_e2e(self, flat, steps, warmup, barrier):
+        torch = self.torch
+        dev = self.dp.device
+        h_c = torch.from_numpy(self.shard_coeffs(flat)).pin_memory()
+        n = self.n
+        h_g = torch.empty((2 * self.rc, 4 * n - 1), dtype=torch.complex128).pin_memory()
+        h_b = torch.empty_like(h_c).pin_memory()
+        d_c = torch.empty(h_c.shape, dtype=torch.complex128, device=dev)
+        d_g = torch.empty(h_g.shape, dtype=torch.complex128, device=dev)
+        d_b = torch.empty_like(d_c)
+
+        def step():
+            d_c.copy_(h_c, non_blocking=True)
+            self.forward(d_c, d_g)
+            h_g.copy_(d_g, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            d_g.copy_(h_g, non_blocking=True)
+            self.inverse(d_g, d_b)
+            h_b.copy_(d_b, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(warmup):
+            step()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        barrier()
+        return {"ms": e0.elapsed_time(e1) / steps,
+                "h2d": (h_c.numel() + h_g.numel()) * 16,
+                "d2h": (h_g.numel() + h_c.numel()) * 16}
+
+
+def _flat_offset(n, m):
+    """Start of order m in ShtCoeffs.pack() (m ascending from -(2N-1))."""
+    k = 2 * n
+    if m <= 0:
+        return (k + m - 1) * (k + m) // 2
+    return (k - 1) * k // 2 + m * k - m * (m - 1) // 2

@@ -342,8 +342,44 @@ class ShtPlan:
         return self.alt_plans[0].quadrature
 
 
+class _ArrRef:
+    """Placeholder for an array spilled to a shared scratch file."""
+
+    __slots__ = ("off", "shape", "dtype")
+
+    def __init__(self, off, shape, dtype):
+        self.off, self.shape, self.dtype = off, shape, dtype
+
+
+def _spill_dir():
+    # tmpfs when it has room for the payloads, else the regular temp dir
+    try:
+        st = os.statvfs("/dev/shm")
+        if st.f_bavail * st.f_frsize > (8 << 30):
+            return "/dev/shm"
+    except OSError:
+        pass
+    import tempfile
+    return tempfile.gettempdir()
+
+
+def _map_payloads(plans, fn):
+    """Apply fn to every payload array of every plan, in place."""
+    for pl in plans:
+        for blocks in (pl.blocks_odd, pl.blocks_even):
+            for blk in blocks:
+                p = blk.payload
+                if isinstance(p, ButterflyFactorization):
+                    for f in p.factors:
+                        f.rows, f.cols, f.vals = fn(f.rows), fn(f.cols), fn(f.vals)
+                elif isinstance(p, LowRankFactor):
+                    p.u, p.s, p.v = fn(p.u), fn(p.s), fn(p.v)
+                else:
+                    blk.payload = fn(p)
+
+
 def _plan_orders(args):
-    n, orders, params, n0, tau = args
+    n, orders, params, n0, tau, spill = args
     quadrature = gauss_legendre(2 * n)
     out = []
     for m in orders:
@@ -353,44 +389,94 @@ def _plan_orders(args):
         except Exception as exc:
             raise RuntimeError(f"planning failed at order m={m}: {exc}") \
                 from exc
-    return out
+    if spill is None:
+        return out, None
+    # ship payloads through a shared file instead of the result pipe: the
+    # parent maps it, so N=1024's ~17 GB of payload is never pickled
+    path = os.path.join(spill, f"bfsht_plan_{os.getpid()}_{orders[0]}.bin")
+    with open(path, "wb") as fh:
+        pos = [0]
+
+        def put(a):
+            a = np.ascontiguousarray(a)
+            ref = _ArrRef(pos[0], a.shape, a.dtype.str)
+            if a.nbytes:
+                fh.write(memoryview(a.reshape(-1)).cast("B"))
+            pad = (-a.nbytes) % 64
+            if pad:
+                fh.write(b"\0" * pad)
+            pos[0] += a.nbytes + pad
+            return ref
+
+        _map_payloads(out, put)
+    for pl in out:
+        for spec in (pl.spec_odd, pl.spec_even):
+            if spec is not None:
+                spec.quadrature = None
+    return out, path
 
 
-def plan_sht(n, params=None, n0=None, tau=TAU_DEFAULT, processes=1):
-    """Plans for every order m = 0..2N-1 sharing one quadrature rule
-    (sht.py:109-128).  ``processes > 1`` plans orders in parallel host
-    processes (orders dealt round-robin, which balances cost)."""
-    if n < 1:
-        raise ValueError("n must be >= 1")
+def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
+                processes=1, quadrature=None):
+    """Plans for an arbitrary list of orders (one shard of an SHT), built in
+    ``processes`` host processes (0/None = all cores); orders are dealt
+    round-robin, which balances cost because it falls with m."""
+    orders = [int(m) for m in orders]
     if params is None:
         params = SamplingConfig()
     n0 = N0_DEFAULT if n0 is None else n0
-    quadrature = gauss_legendre(2 * n)
-    if processes is None or processes < 0:
+    if quadrature is None:
+        quadrature = gauss_legendre(2 * n)
+    if not processes or processes < 0:
         processes = os.cpu_count() or 1
-    if processes <= 1 or n < 8:
+    p = min(processes, len(orders))
+    if p <= 1:
         plans = []
-        for m in range(2 * n):
+        for m in orders:
             try:
                 plans.append(plan_alt(n, m, params, n0=n0, tau=tau,
                                       quadrature=quadrature))
             except Exception as exc:
                 raise RuntimeError(
                     f"planning failed at order m={m}: {exc}") from exc
-    else:
-        import multiprocessing as mp
-        ctx = mp.get_context("fork")
-        p = min(processes, 2 * n)
-        chunks = [list(range(r, 2 * n, p)) for r in range(p)]
-        with ctx.Pool(p) as pool:
-            res = pool.map(_plan_orders,
-                           [(n, c, params, n0, tau) for c in chunks])
-        plans = [None] * (2 * n)
-        for chunk, got in zip(chunks, res):
-            for m, pl in zip(chunk, got):
-                plans[m] = pl
-        for pl in plans:
+        return plans
+    import multiprocessing as mp
+    ctx = mp.get_context("fork")
+    chunks = [orders[r::p] for r in range(p)]
+    spill = _spill_dir()
+    with ctx.Pool(p) as pool:
+        res = pool.map(_plan_orders,
+                       [(n, c, params, n0, tau, spill) for c in chunks])
+    by_m = {}
+    for chunk, (got, path) in zip(chunks, res):
+        if path is not None:
+            mm = np.memmap(path, dtype=np.uint8, mode="r")
+            os.unlink(path)   # the mapping keeps the pages alive
+
+            def get(ref, mm=mm):
+                dt = np.dtype(ref.dtype)
+                count = int(np.prod(ref.shape)) if ref.shape else 1
+                return np.frombuffer(mm, dtype=dt, count=count,
+                                     offset=ref.off).reshape(ref.shape)
+
+            _map_payloads(got, get)
+        for m, pl in zip(chunk, got):
             for spec in (pl.spec_odd, pl.spec_even):
                 if spec is not None:
                     spec.quadrature = quadrature
+            by_m[m] = pl
+    return [by_m[m] for m in orders]
+
+
+def plan_sht(n, params=None, n0=None, tau=TAU_DEFAULT, processes=1):
+    """Plans for every order m = 0..2N-1 sharing one quadrature rule
+    (sht.py:109-128).  ``processes > 1`` plans orders in parallel host
+    processes."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if params is None:
+        params = SamplingConfig()
+    if processes is not None and processes > 1 and n < 8:
+        processes = 1
+    plans = plan_orders(n, range(2 * n), params, n0, tau, processes)
     return ShtPlan(n=n, alt_plans=plans, params=params)
