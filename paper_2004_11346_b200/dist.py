@@ -49,6 +49,74 @@ def _stream(torch):
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+class ExchangePlan:
+    """Host-side layout of the per-direction all-to-all (no device code).
+
+    send side: for each destination rank q (row pairs rows[q]), the node-half
+    entries of this rank's orders, order by order, odd then even half, rows
+    ascending — as arena entry indices (``send_idx``) and per-destination
+    counts.  receive side: the same chunks from every source rank s, laid
+    out so that entry (m, parity, r) sits at recv_halves[2m+parity].y +
+    (r - r0): the layout the DFT kernels read.
+    """
+
+    def __init__(self, n, world, rank, halves):
+        self.n, self.world, self.rank = n, world, rank
+        self.all_orders = lpt_orders(n, world)
+        self.orders = self.all_orders[rank]
+        self.rows = row_split(n, world)
+        self.r0 = self.rows[rank][0]
+        self.rc = self.rows[rank][1] - self.r0
+        h = np.asarray(halves)
+        if len(h) != 2 * len(self.orders) or \
+                list(h["m"][0::2]) != list(self.orders):
+            raise ValueError("halves do not match this rank's orders")
+        send_idx, self.send_counts = [], []
+        for a, b in self.rows:
+            cnt = 0
+            for o in range(len(self.orders)):
+                for par in range(2):
+                    hf = h[2 * o + par]
+                    if hf["ncols"] == 0:
+                        continue
+                    send_idx.append(np.arange(hf["y"] + a, hf["y"] + b,
+                                              dtype=np.int32))
+                    cnt += b - a
+            self.send_counts.append(cnt)
+        self.send_idx = np.concatenate(send_idx) if send_idx \
+            else np.zeros(0, np.int32)
+        self.recv_halves = np.zeros(4 * n, dtype=HALF_DTYPE)
+        self.recv_counts = []
+        pos = 0
+        for s in range(world):
+            cnt = 0
+            for m in self.all_orders[s]:
+                for par in range(2):
+                    hf = self.recv_halves[2 * m + par]
+                    hf["m"] = m
+                    nc = half_cols(n, m, par)
+                    hf["ncols"] = nc
+                    if nc == 0:
+                        continue
+                    hf["y"] = pos
+                    pos += self.rc
+                    cnt += self.rc
+            self.recv_counts.append(cnt)
+        self.recv_entries = pos
+        offs, at = [], 0
+        for m in self.orders:
+            offs.append(at)
+            at += (2 * n - m) * (2 if m else 1)
+        self.coeff_offsets = np.array(offs + [at], dtype=np.int64)
+        self.coeff_len = at
+
+
+def half_cols(n, m, par):
+    """Columns of the (m, parity) half; 0 when absent (alt.py:102-107)."""
+    half = (m + 1) // 2 if par == 0 else m // 2
+    return max(n - half, 0)
+
+
 class _Common:
     def launches_total(self):
         return int(self.dp.lib.bfsht_plan_launches(self.dp.handle))
@@ -168,63 +236,20 @@ class ShardedSht(_Common):
         lib = self.dp.lib
         self.lib = lib
         dev = self.dp.device
-        # every rank's order list (deterministic, no communication needed)
-        self.all_orders = lpt_orders(n, world)
-        assert self.all_orders[rank] == self.orders, "orders must follow lpt_orders"
-        self.rows = row_split(n, world)
-        r0, r1 = self.rows[rank]
-        self.r0, self.rc = r0, r1 - r0
-        # presence of each (order, parity) half: needs only N and m
-        def ncols(m, par):
-            half = (m + 1) // 2 if par == 0 else m // 2
-            return max(n - half, 0)
-
-        # --- send side: entries of my orders' node halves, by destination
-        h = self.dp.packed.halves
-        send_idx, send_counts = [], []
-        for q in range(world):
-            a, b = self.rows[q]
-            cnt = 0
-            for o in range(len(self.orders)):
-                for par in range(2):
-                    hf = h[2 * o + par]
-                    if hf["ncols"] == 0:
-                        continue
-                    send_idx.append(np.arange(hf["y"] + a, hf["y"] + b, dtype=np.int32))
-                    cnt += b - a
-            send_counts.append(cnt)
-        self.send_idx = torch.from_numpy(np.concatenate(send_idx) if send_idx
-                                         else np.zeros(0, np.int32)).to(dev)
-        self.send_counts = send_counts
-        # --- receive side: my row pairs for every order, chunked by source
-        recv_halves = np.zeros(4 * n, dtype=HALF_DTYPE)
-        recv_counts = []
-        pos = 0
-        for s in range(world):
-            cnt = 0
-            for m in self.all_orders[s]:
-                for par in range(2):
-                    recv_halves[2 * m + par]["m"] = m
-                    nc = ncols(m, par)
-                    recv_halves[2 * m + par]["ncols"] = nc
-                    if nc == 0:
-                        continue
-                    recv_halves[2 * m + par]["y"] = pos
-                    pos += self.rc
-                    cnt += self.rc
-            recv_counts.append(cnt)
-        self.recv_counts = recv_counts
-        self.recv_entries = pos
-        self.recv_halves = torch.from_numpy(recv_halves.view(np.int32).copy()).to(dev)
-        self.sendbuf = torch.zeros((max(sum(send_counts), 1), NRHS), dtype=torch.float64, device=dev)
-        self.recvbuf = torch.zeros((max(pos, 1), NRHS), dtype=torch.float64, device=dev)
-        # coefficient shard offsets: +m then -m per local order
-        offs, at = [], 0
-        for m in self.orders:
-            offs.append(at)
-            at += (2 * n - m) * (2 if m else 1)
-        self.coeff_len = at
-        self.coeff_off = torch.tensor(offs + [at], dtype=torch.int64, device=dev)
+        xp = ExchangePlan(n, world, rank, self.dp.packed.halves)
+        self.xp = xp
+        self.all_orders, self.rows = xp.all_orders, xp.rows
+        self.r0, self.rc = xp.r0, xp.rc
+        self.send_idx = torch.from_numpy(xp.send_idx).to(dev)
+        self.send_counts, self.recv_counts = xp.send_counts, xp.recv_counts
+        self.recv_entries = xp.recv_entries
+        self.recv_halves = torch.from_numpy(xp.recv_halves.view(np.int32).copy()).to(dev)
+        self.sendbuf = torch.zeros((max(sum(xp.send_counts), 1), NRHS),
+                                   dtype=torch.float64, device=dev)
+        self.recvbuf = torch.zeros((max(xp.recv_entries, 1), NRHS),
+                                   dtype=torch.float64, device=dev)
+        self.coeff_len = xp.coeff_len
+        self.coeff_off = torch.from_numpy(xp.coeff_offsets).to(dev)
         self.weights = self.dp.weights
 
     def make_buffers(self, flat):
