@@ -77,8 +77,8 @@ int bfsht_pack_plan(const bfsht_manifest *man, int threads,
 /* Sizes and host pointers of the packed arrays (for upload / inspection).
  * info[]: 0 tile doubles, 1 ops, 2 idx, 3 lane maps, 4 tasks,
  * 5 arena entries, 6 halves, 7 stages fwd, 8 stages inv,
- * 9 payload values (sum of stored reference values), 10 stored tile doubles
- * incl. zero fill, 11 butterfly blocks, 12 low-rank blocks, 13 dense blocks,
+ * 9 payload values (sum of stored reference values), 10 arena entry of the
+ * row-major forward node array Yr[r][order][parity], 11 butterfly blocks, 12 low-rank blocks, 13 dense blocks,
  * 14 half-size N, 15 number of order plans */
 int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]);
 int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]);
@@ -105,6 +105,8 @@ double *bfsht_plan_arena(bfsht_plan *pl);
 /* Run every ALT stage of one direction over the arena (inputs already in
  * the arena: coefficient halves for FORWARD, node halves for INVERSE). */
 int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream);
+/* One stage of one direction (stages run in order; for profiling). */
+int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream);
 
 /* Per-order ALT boundary (alt_forward / alt_inverse for one or more plans):
  * in/out are device complex128 buffers laid out plan after plan, lengths

@@ -25,6 +25,8 @@ def declare(lib):
     lib.bfsht_plan_launches.argtypes = [_P]
     lib.bfsht_alt_apply.restype = _I
     lib.bfsht_alt_apply.argtypes = [_P, _I, _P]
+    lib.bfsht_alt_stage.restype = _I
+    lib.bfsht_alt_stage.argtypes = [_P, _I, _I, _P]
     lib.bfsht_alt_orders.restype = _I
     lib.bfsht_alt_orders.argtypes = [_P, _I, _P, _P, _P, _P]
     lib.bfsht_sht_forward.restype = _I
@@ -52,7 +54,7 @@ EXPORTS = (
     "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
     "bfsht_packed_free", "bfsht_last_error", "bfsht_plan_upload",
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
-    "bfsht_alt_apply", "bfsht_alt_orders", "bfsht_sht_forward",
+    "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_sht_forward",
     "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
     "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",
     "bfsht_gather_entries", "bfsht_scatter_entries", "bfsht_synth_rows",

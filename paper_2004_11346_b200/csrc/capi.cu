@@ -41,6 +41,27 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
     pl->owned.push_back(pl->order_off);
     BF_CUDA(cudaMemcpy(pl->order_off, off.data(), sizeof(int64_t) * (pl->norders + 1),
                        cudaMemcpyHostToDevice));
+    // DFT-stage addressing of node halves (see engine.cuh)
+    {
+        std::vector<bf_half> lf(nh), li(nh);
+        const int32_t stride = 2 * pl->norders;
+        for (int64_t h = 0; h < nh; ++h) {
+            lf[h] = li[h] = host_halves[h];
+            lf[h].x = stride;
+            lf[h].y = (int32_t)pl->info[10] + (int32_t)h;
+            li[h].x = 1;
+        }
+        BF_CUDA(cudaMalloc(&pl->layout_fwd, sizeof(bf_half) * (nh ? nh : 1)));
+        pl->owned.push_back(pl->layout_fwd);
+        BF_CUDA(cudaMalloc(&pl->layout_inv, sizeof(bf_half) * (nh ? nh : 1)));
+        pl->owned.push_back(pl->layout_inv);
+        if (nh) {
+            BF_CUDA(cudaMemcpy(pl->layout_fwd, lf.data(), sizeof(bf_half) * nh,
+                               cudaMemcpyHostToDevice));
+            BF_CUDA(cudaMemcpy(pl->layout_inv, li.data(), sizeof(bf_half) * nh,
+                               cudaMemcpyHostToDevice));
+        }
+    }
     pl->ncounters = (int)std::max(pl->info[7], pl->info[8]) + 1;
     BF_CUDA(cudaMalloc(&pl->counters, sizeof(int) * pl->ncounters));
     pl->owned.push_back(pl->counters);
@@ -154,6 +175,19 @@ int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream) {
     }
 
     return bf_alt_apply(pl, dir, (cudaStream_t)stream);
+}
+
+int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
+    if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan or direction";
+        return -1;
+    }
+    const std::vector<int64_t> &b = pl->stages[dir];
+    if (stage < 0 || stage + 1 >= (int)b.size()) {
+        g_err = "stage out of range";
+        return -1;
+    }
+    return bf_run_stage(pl, b[stage], b[stage + 1], pl->counters + stage, (cudaStream_t)stream);
 }
 
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,

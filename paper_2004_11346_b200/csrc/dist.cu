@@ -69,8 +69,10 @@ __global__ void scatter_entries_kernel(double4 *__restrict__ arena,
                                        const int32_t *__restrict__ idx, int64_t count,
                                        const double4 *__restrict__ in) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x)
-        arena[idx[i]] = in[i];
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t t = idx[i];
+        if (t >= 0) arena[t] = in[i];   // -1: absent half, nothing to write
+    }
 }
 
 int grid_for(int64_t count) {

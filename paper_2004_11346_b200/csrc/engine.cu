@@ -7,19 +7,25 @@
 //
 // Execution model (sm_100a):
 //  * grid = one CTA per SM, 8 warps per CTA; every warp is an independent
-//    worker that claims tasks from a global counter (tasks are pre-sorted by
-//    cost, so this is longest-first list scheduling).
-//  * a task accumulates <= 32 output entries x 4 RHS in registers (lane =
-//    output entry) over its ops, then stores them once: no atomics, fixed
-//    summation order, bitwise-reproducible results.
-//  * each warp owns a 3-slot shared-memory ring.  Lane 0 streams the next
-//    ops' tiles (and contiguous input vectors) with 1-D TMA bulk copies
+//    worker that walks the stage's task list (pre-sorted by cost) as one
+//    flat op stream, claiming tasks from a global counter one task ahead.
+//  * a task accumulates <= 32 output entries x 4 RHS in registers, then
+//    stores them once: no atomics, fixed summation order, bitwise-
+//    reproducible results.
+//  * each warp owns a 3-slot shared-memory ring.  Lane 0 streams tiles (and
+//    contiguous input vectors) with 1-D TMA bulk copies
 //    (cp.async.bulk ... mbarrier::complete_tx), all lanes gather indexed
 //    input entries with cp.async into the same slot, and the slot's
-//    mbarrier completes when both have landed.  Payload bytes are read from
-//    HBM exactly once per direction; all reuse (4 RHS per value) is from
-//    shared memory, conflict-free thanks to the rotated tile layout.
+//    mbarrier completes when both have landed.  Op descriptors and gather
+//    indices are prefetched one step ahead so no dependent global load sits
+//    between a consumed op and the next issue.
+//  * tile products run on the fp64 tensor cores: mma.sync.m8n8k4.f64 with
+//    the 4 RHS in the n dimension (n = 8, half used).  A 32x32 tile costs 32
+//    DMMA + 40 fragment loads instead of ~650 scalar instructions, which is
+//    what keeps the kernel on the HBM roofline rather than issue-bound.
+//    Payload bytes are read from HBM exactly once per direction.
 #include <cuda_runtime.h>
+#include <stddef.h>
 #include <stdint.h>
 
 #include "engine.cuh"
@@ -34,6 +40,10 @@ constexpr int kVecDoubles = BF_T * BF_NRHS;
 struct alignas(128) WarpRing {
     double tile[kStages][kTileDoubles];
     double vec[kStages][kVecDoubles];
+    double scratch[kVecDoubles];    // op result staging for remapped outputs
+    double zero[16];                // stands in for blocks past a tile edge
+    bf_op meta[kStages];            // op descriptor of the slot's op
+    int4 tmeta[kStages];            // task out, nout|stride<<8, last-op-of-task
     unsigned long long full[kStages];
 };
 
@@ -86,6 +96,14 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// D(8x8) += A(8x4) * B(4x8), fp64 tensor core.  Lane l holds A[l/4][l%4],
+// B[l%4][l/4], D[l/4][2(l%4)], D[l/4][2(l%4)+1].
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
 struct StageArgs {
     const double *tiles;
     const bf_op *ops;
@@ -96,52 +114,6 @@ struct StageArgs {
     int64_t t0, ntasks;
     int *counter;
 };
-
-// Issue the loads of one op into ring slot `s` (whole warp).
-__device__ __forceinline__ void issue_op(const StageArgs &a, WarpRing &ring, int s,
-                                         const bf_op &op, int lane) {
-    const double *arena = a.arena;
-    uint32_t bytes = 0;
-    int nvec = 0;
-    bool gather = (op.flags & BF_OPF_GATHER) != 0;
-    if (op.kind == BF_OP_ADD) {
-        // entries for lanes [off, off+R)
-        int j = lane - op.off;
-        if (j >= 0 && j < op.R) {
-            int src = gather ? __ldg(a.idx + op.in + j) : op.in + j;
-            if (src >= 0) {
-                const double *g = arena + (int64_t)src * BF_NRHS;
-                cp_async16(&ring.vec[s][lane * BF_NRHS], g);
-                cp_async16(&ring.vec[s][lane * BF_NRHS + 2], g + 2);
-            }
-        }
-    } else {
-        nvec = (op.kind == BF_OP_TILE_N) ? op.C : op.R;
-        bytes = (((uint32_t)op.R * op.C * 8u) + 15u) & ~15u;
-        if (gather) {
-            if (lane < nvec) {
-                int src = __ldg(a.idx + op.in + lane);
-                const double *g = arena + (int64_t)src * BF_NRHS;
-                cp_async16(&ring.vec[s][lane * BF_NRHS], g);
-                cp_async16(&ring.vec[s][lane * BF_NRHS + 2], g + 2);
-            }
-        } else {
-            bytes += (uint32_t)nvec * BF_NRHS * 8u;
-        }
-    }
-    cp_async_arrive(&ring.full[s]);
-    if (lane == 0) {
-        fence_proxy_async();
-        mbar_arrive_tx(&ring.full[s], bytes);
-        if (op.kind != BF_OP_ADD) {
-            uint32_t tb = (((uint32_t)op.R * op.C * 8u) + 15u) & ~15u;
-            bulk_g2s(ring.tile[s], a.tiles + op.tile, tb, &ring.full[s]);
-            if (!gather)
-                bulk_g2s(ring.vec[s], arena + (int64_t)op.in * BF_NRHS,
-                         (uint32_t)nvec * BF_NRHS * 8u, &ring.full[s]);
-        }
-    }
-}
 
 __device__ __forceinline__ bf_op load_op(const bf_op *p) {
     // 24-byte record, 8-byte aligned: three 8-byte loads
@@ -154,105 +126,364 @@ __device__ __forceinline__ bf_op load_op(const bf_op *p) {
     return o;
 }
 
+// One op in flight through the per-warp pipeline (uniform across lanes).
+struct Rec {
+    bf_op op;
+    int out, nout, last, valid;
+};
+
+// Walks the global task list as one flat op stream, one op per call.  The
+// next task is claimed one task ahead so that the claim (atomicAdd) and the
+// task-record load are off the critical path.
+struct Cursor {
+    int base, n, i, out, nout;   // current task
+    int nt;                      // next claimed task id
+    bf_task ntask;               // its record (valid when nt < ntasks)
+};
+
+__device__ __forceinline__ int claim(const StageArgs &a, int lane) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(a.counter, 1);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+
+__device__ __forceinline__ bf_task load_task(const StageArgs &a, int t) {
+    const int4 v = __ldg(reinterpret_cast<const int4 *>(a.tasks + a.t0 + t));
+    bf_task k;
+    k.op_begin = v.x;
+    k.op_count = v.y;
+    k.out = v.z;
+    k.nout = v.w;
+    return k;
+}
+
+__device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) {
+    Rec r;
+    r.valid = 0;
+    if (c.i >= c.n) {
+        if (c.nt >= a.ntasks) return r;
+        c.base = c.ntask.op_begin;
+        c.n = c.ntask.op_count;
+        c.out = c.ntask.out;
+        c.nout = c.ntask.nout;
+        c.i = 0;
+        c.nt = claim(a, lane);
+        if (c.nt < a.ntasks) c.ntask = load_task(a, c.nt);
+    }
+    r.op = load_op(a.ops + c.base + c.i);
+    r.out = c.out;
+    r.nout = c.nout;
+    r.last = (c.i == c.n - 1);
+    r.valid = 1;
+    ++c.i;
+    return r;
+}
+
+// gather source of this lane for op r (-1: none); loaded one step early
+__device__ __forceinline__ int gather_src(const StageArgs &a, const Rec &r, int lane) {
+    if (!r.valid || !(r.op.flags & BF_OPF_GATHER)) return -1;
+    if (r.op.kind == BF_OP_ADD) {
+        const int j = lane - r.op.off;
+        return (j >= 0 && j < r.op.R) ? __ldg(a.idx + r.op.in + j) : -1;
+    }
+    const int nvec = (r.op.kind == BF_OP_TILE_N) ? r.op.C : r.op.R;
+    return lane < nvec ? __ldg(a.idx + r.op.in + lane) : -1;
+}
+
+__device__ __forceinline__ uint32_t tile_bytes(const bf_op &op) {
+    return (uint32_t)bf_tile_doubles(op.R, op.C) * 8u;
+}
+
+// Issue the loads of one op into ring slot s (whole warp).
+__device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s, const Rec &r,
+                                      int gsrc, int lane) {
+    const bf_op &op = r.op;
+    const double *arena = a.arena;
+    const bool gather = (op.flags & BF_OPF_GATHER) != 0;
+    if (lane == 0) {
+        ring.meta[s] = op;
+        ring.tmeta[s] = make_int4(r.out, r.nout, r.last, 0);
+    }
+    uint32_t bytes = 0;
+    int nvec = 0;
+    int src = -1;
+    if (op.kind == BF_OP_ADD) {
+        const int j = lane - op.off;
+        if (j >= 0 && j < op.R) src = gather ? gsrc : op.in + j;
+    } else {
+        nvec = (op.kind == BF_OP_TILE_N) ? op.C : op.R;
+        bytes = tile_bytes(op);
+        if (gather)
+            src = gsrc;
+        else
+            bytes += (uint32_t)nvec * BF_NRHS * 8u;
+    }
+    if (src >= 0 && (gather || op.kind == BF_OP_ADD)) {
+        const double *gp = arena + (int64_t)src * BF_NRHS;
+        cp_async16(&ring.vec[s][lane * BF_NRHS], gp);
+        cp_async16(&ring.vec[s][lane * BF_NRHS + 2], gp + 2);
+    } else if (op.kind == BF_OP_ADD) {
+        // lanes without a source add zeros (keeps index loads off the consumer)
+        *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS]) = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS + 2]) = make_double2(0.0, 0.0);
+    }
+    cp_async_arrive(&ring.full[s]);
+    if (lane == 0) {
+        fence_proxy_async();
+        mbar_arrive_tx(&ring.full[s], bytes);
+        if (op.kind != BF_OP_ADD) {
+            bulk_g2s(ring.tile[s], a.tiles + op.tile, tile_bytes(op), &ring.full[s]);
+            if (!gather)
+                bulk_g2s(ring.vec[s], arena + (int64_t)op.in * BF_NRHS,
+                         (uint32_t)nvec * BF_NRHS * 8u, &ring.full[s]);
+        }
+    }
+}
+
+// Tile product of one op into fragments e: e[mt][0..1] = result row
+// 8mt + lane/4, RHS 2(lane%4), 2(lane%4)+1 (lanes with lane%4 >= 2 carry the
+// n-padding and stay zero).
+__device__ __forceinline__ void tile_product(const bf_op &op, const double *T, const double *V,
+                                             const double *Z, int lane, double e[4][2]) {
+    const int g = lane >> 2, q = lane & 3, hi = lane >> 4;
+    const int R4 = (op.R + 3) >> 2, C4 = (op.C + 3) >> 2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) e[mt][0] = e[mt][1] = 0.0;
+    // B fragment: lane holds V[k = 4ks + q][rhs = g] (rhs 4..7 are the n-padding)
+    const bool bl = g < 4;
+    const double *Vb = V + q * 4 + (g & 3);
+    if (op.R == BF_T && op.C == BF_T) {
+        // full tile: straight-line, all fragment offsets are immediates
+        if (op.kind == BF_OP_TILE_N) {
+            const double *Ta = T + hi * (8 * 16) + (lane & 15);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+                    dmma(e[mt][0], e[mt][1], Ta[(mt * 16 + ks) * 16], b);
+            }
+        } else {
+            const double *Ta = T + hi * 16 + q * 4 + (g & 3);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+                    dmma(e[mt][0], e[mt][1], Ta[(ks * 8 + 2 * mt) * 16], b);
+            }
+        }
+        return;
+    }
+    // partial tile: per-lane fragment pointers walk the k blocks; block rows
+    // (N) / block columns (T) past the tile edge read a zero block instead,
+    // so the k loop carries no predicates
+    const double *p[4];
+    int st[4];
+    int K, MT;
+    if (op.kind == BF_OP_TILE_N) {
+        // y = A x: result rows = tile rows, k over tile column blocks
+        K = C4;
+        MT = (op.R + 7) >> 3;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int br = 2 * mt + hi;
+            const bool ok = br < R4;
+            p[mt] = (ok ? T + br * C4 * 16 : Z) + (lane & 15);
+            st[mt] = ok ? 16 : 0;
+        }
+    } else {
+        // x = A^T y: result rows = tile columns, k over tile row blocks
+        K = R4;
+        MT = (op.C + 7) >> 3;
+        const int inblk = q * 4 + (g & 3);
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int bc = 2 * mt + hi;
+            const bool ok = bc < C4;
+            p[mt] = (ok ? T + bc * 16 : Z) + inblk;
+            st[mt] = ok ? C4 * 16 : 0;
+        }
+    }
+    switch (MT) {
+        case 4:
+            for (int ks = 0; ks < K; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    dmma(e[mt][0], e[mt][1], *p[mt], b);
+                    p[mt] += st[mt];
+                }
+            }
+            break;
+        case 3:
+            for (int ks = 0; ks < K; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 3; ++mt) {
+                    dmma(e[mt][0], e[mt][1], *p[mt], b);
+                    p[mt] += st[mt];
+                }
+            }
+            break;
+        case 2:
+            for (int ks = 0; ks < K; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    dmma(e[mt][0], e[mt][1], *p[mt], b);
+                    p[mt] += st[mt];
+                }
+            }
+            break;
+        default:
+            for (int ks = 0; ks < K; ++ks) {
+                const double b = bl ? Vb[ks * 16] : 0.0;
+                dmma(e[0][0], e[0][1], *p[0], b);
+                p[0] += st[0];
+            }
+            break;
+    }
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpRing &ring = reinterpret_cast<WarpRing *>(smem_raw)[warp];
+    {
+        // zero the ring once: padded tile columns multiply stale vector
+        // entries, which must therefore be finite
+        double2 *z = reinterpret_cast<double2 *>(&ring);
+        const int n2 = (int)(offsetof(WarpRing, meta) / sizeof(double2));
+        for (int i = lane; i < n2; i += 32) z[i] = make_double2(0.0, 0.0);
+    }
     if (lane == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&ring.full[s], 33);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
+    const int g = lane >> 2, q = lane & 3;
+
+    Cursor cur;
+    cur.n = cur.i = 0;
+    cur.base = cur.out = cur.nout = 0;
+    cur.nt = claim(a, lane);
+    if (cur.nt < a.ntasks) cur.ntask = load_task(a, cur.nt);
+
+    Rec q0 = advance(a, cur, lane);
+    int g0 = gather_src(a, q0, lane);
+    Rec q1 = advance(a, cur, lane);
     uint32_t seq_issue = 0, seq_use = 0;
+    for (int s = 0; s < kStages && q0.valid; ++s) {
+        issue(a, ring, seq_issue % kStages, q0, g0, lane);
+        ++seq_issue;
+        q0 = q1;
+        g0 = gather_src(a, q0, lane);
+        q1 = advance(a, cur, lane);
+    }
 
-    for (;;) {
-        int t = 0;
-        if (lane == 0) t = atomicAdd(a.counter, 1);
-        t = __shfl_sync(0xffffffffu, t, 0);
-        if (t >= a.ntasks) break;
-        const bf_task task = a.tasks[a.t0 + t];
-        const bf_op *ops = a.ops + task.op_begin;
-        const int nops = task.op_count;
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+    // task accumulator: acc[j] = slot 8j + lane/4, RHS 2(lane%4) .. +1
+    double acc[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
 
-        int issued = 0;
-        for (; issued < nops && issued < kStages; ++issued) {
-            bf_op op = load_op(ops + issued);
-            issue_op(a, ring, seq_issue % kStages, op, lane);
-            ++seq_issue;
-        }
-        for (int i = 0; i < nops; ++i) {
-            const int s = seq_use % kStages;
-            mbar_wait(&ring.full[s], (seq_use / kStages) & 1u);
-            ++seq_use;
-            const bf_op op = load_op(ops + i);
-            const double *T = ring.tile[s];
-            const double *V = ring.vec[s];
-            if (op.kind == BF_OP_ADD) {
-                int j = lane - op.off;
-                if (j >= 0 && j < op.R) {
-                    int src = (op.flags & BF_OPF_GATHER) ? __ldg(a.idx + op.in + j) : 0;
-                    if (src >= 0) {
-                        double2 v01 = *reinterpret_cast<const double2 *>(V + lane * 4);
-                        double2 v23 = *reinterpret_cast<const double2 *>(V + lane * 4 + 2);
-                        acc0 += v01.x; acc1 += v01.y; acc2 += v23.x; acc3 += v23.y;
-                    }
+    while (seq_use < seq_issue) {
+        const int s = seq_use % kStages;
+        mbar_wait(&ring.full[s], (seq_use / kStages) & 1u);
+        ++seq_use;
+        const bf_op op = ring.meta[s];
+        const int4 tm = ring.tmeta[s];
+        const double *V = ring.vec[s];
+        if (op.kind == BF_OP_ADD) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sl = 8 * j + g;
+                const int jj = sl - op.off;
+                if (q < 2 && jj >= 0 && jj < op.R) {
+                    const double2 v = *reinterpret_cast<const double2 *>(V + sl * 4 + 2 * q);
+                    acc[j][0] += v.x;
+                    acc[j][1] += v.y;
+                }
+            }
+        } else {
+            double e[4][2];
+            tile_product(op, ring.tile[s], V, ring.zero, lane, e);
+            const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
+            if (!lanemap && (op.off & 7) == 0) {
+                // result m-tile mt lands on slot m-tile mt + off/8
+                // (explicit cases keep acc and e in registers)
+                switch (op.off >> 3) {
+                    case 0:
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            acc[j][0] += e[j][0];
+                            acc[j][1] += e[j][1];
+                        }
+                        break;
+                    case 1:
+#pragma unroll
+                        for (int j = 1; j < 4; ++j) {
+                            acc[j][0] += e[j - 1][0];
+                            acc[j][1] += e[j - 1][1];
+                        }
+                        break;
+                    case 2:
+#pragma unroll
+                        for (int j = 2; j < 4; ++j) {
+                            acc[j][0] += e[j - 2][0];
+                            acc[j][1] += e[j - 2][1];
+                        }
+                        break;
+                    default:
+                        acc[3][0] += e[0][0];
+                        acc[3][1] += e[0][1];
+                        break;
                 }
             } else {
-                const int R = op.R, C = op.C;
-                double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-                if (op.kind == BF_OP_TILE_N) {
-                    if (lane < R) {
-                        int j = lane;
-                        for (int c = 0; c < C; ++c) {
-                            const double x = T[c * R + j];
-                            const double2 v01 = *reinterpret_cast<const double2 *>(V + c * 4);
-                            const double2 v23 = *reinterpret_cast<const double2 *>(V + c * 4 + 2);
-                            p0 = fma(x, v01.x, p0); p1 = fma(x, v01.y, p1);
-                            p2 = fma(x, v23.x, p2); p3 = fma(x, v23.y, p3);
-                            j = (j + 1 == R) ? 0 : j + 1;
-                        }
-                    }
-                } else {
-                    if (lane < C) {
-                        int j = lane % R;
-                        const double *col = T + lane * R;
-                        for (int r = 0; r < R; ++r) {
-                            const double x = col[j];
-                            const double2 v01 = *reinterpret_cast<const double2 *>(V + r * 4);
-                            const double2 v23 = *reinterpret_cast<const double2 *>(V + r * 4 + 2);
-                            p0 = fma(x, v01.x, p0); p1 = fma(x, v01.y, p1);
-                            p2 = fma(x, v23.x, p2); p3 = fma(x, v23.y, p3);
-                            j = (j + 1 == R) ? 0 : j + 1;
-                        }
+                // general placement through the warp's scratch rows
+                double *S = ring.scratch;
+                const int width = (op.kind == BF_OP_TILE_N) ? op.R : op.C;
+                const int MT = (width + 7) >> 3;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+                    if (mt < MT && q < 2)
+                        *reinterpret_cast<double2 *>(S + (8 * mt + g) * 4 + 2 * q) =
+                            make_double2(e[mt][0], e[mt][1]);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int sl = 8 * j + g;
+                    const int src = lanemap ? (int)__ldg(a.maps + (int64_t)op.aux * BF_T + sl)
+                                            : sl - op.off;
+                    if (q < 2 && src >= 0 && src < width) {
+                        const double2 v = *reinterpret_cast<const double2 *>(S + src * 4 + 2 * q);
+                        acc[j][0] += v.x;
+                        acc[j][1] += v.y;
                     }
                 }
-                const int width = (op.kind == BF_OP_TILE_N) ? R : C;
-                int src;
-                if (op.flags & BF_OPF_LANEMAP)
-                    src = __ldg(a.maps + (int64_t)op.aux * BF_T + lane);
-                else
-                    src = lane - op.off;
-                const bool ok = src >= 0 && src < width;
-                const int sl = ok ? src : 0;
-                p0 = __shfl_sync(0xffffffffu, p0, sl);
-                p1 = __shfl_sync(0xffffffffu, p1, sl);
-                p2 = __shfl_sync(0xffffffffu, p2, sl);
-                p3 = __shfl_sync(0xffffffffu, p3, sl);
-                if (ok) { acc0 += p0; acc1 += p1; acc2 += p2; acc3 += p3; }
-            }
-            __syncwarp();
-            if (issued < nops) {
-                bf_op nop = load_op(ops + issued);
-                issue_op(a, ring, seq_issue % kStages, nop, lane);
-                ++seq_issue;
-                ++issued;
+                __syncwarp();
             }
         }
-        if (lane < task.nout) {
-            double *o = a.arena + ((int64_t)task.out + lane) * BF_NRHS;
-            *reinterpret_cast<double2 *>(o) = make_double2(acc0, acc1);
-            *reinterpret_cast<double2 *>(o + 2) = make_double2(acc2, acc3);
+        if (tm.z) {
+            const int nout = tm.y & 0xff;
+            const int stride = (tm.y >> 8) ? (tm.y >> 8) : 1;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int sl = 8 * j + g;
+                if (q < 2 && sl < nout) {
+                    double *o = a.arena + ((int64_t)tm.x + (int64_t)sl * stride) * BF_NRHS + 2 * q;
+                    *reinterpret_cast<double2 *>(o) = make_double2(acc[j][0], acc[j][1]);
+                }
+                acc[j][0] = acc[j][1] = 0.0;
+            }
+        }
+        __syncwarp();
+        if (q0.valid) {
+            issue(a, ring, seq_issue % kStages, q0, g0, lane);
+            ++seq_issue;
+            q0 = q1;
+            g0 = gather_src(a, q0, lane);
+            q1 = advance(a, cur, lane);
         }
     }
 }

@@ -17,6 +17,10 @@ struct bfsht_plan {
     const int8_t *maps = nullptr;
     const bf_task *tasks = nullptr;
     const bf_half *halves = nullptr;
+    // node-half addressing for the DFT stage: entry (order o, parity p, row r)
+    // at layout[2o+p].y + r * layout[2o+p].x (fwd: row-major Yr; inv: halves)
+    bf_half *layout_fwd = nullptr;
+    bf_half *layout_inv = nullptr;
     double *arena = nullptr;
     std::vector<int64_t> stages[2];   // task bounds per stage (host)
     int32_t n = 0;                    // half size N

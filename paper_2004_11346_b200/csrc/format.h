@@ -5,10 +5,13 @@
  * Every payload value of a plan (dense turning blocks, low-rank u*diag(s)
  * and v, butterfly ID interpolation blocks and middle skeleton blocks)
  * lives in one fp64 "tile store" as R x C tiles (R, C <= 32), each tile
- * contiguous and 16-byte aligned, element (r, c) at c*R + (r + c) % R.
- * That rotation makes both tile products conflict-free from shared memory:
- *   N-mode  lane r: sum_c A[r][c] * v[c]   (apply)
- *   T-mode  lane c: sum_r A[r][c] * v[r]   (apply transpose)
+ * contiguous and 128-byte aligned, stored as 4x4 blocks (zero padded to
+ * multiples of 4): block (r/4, c/4) at ((r/4)*C4 + c/4)*16, element
+ * (r%4)*4 + c%4 inside it.  Every fp64 tensor-core fragment load
+ * (mma.m8n8k4.f64) then touches one 128-byte block per half-warp, for the
+ * A operand of both tile products:
+ *   N-mode  y += A x     (apply)
+ *   T-mode  x += A^T y   (apply transpose)
  * so one stored copy serves the forward ALT (A x) and the inverse ALT
  * (A^T y) — the reference's "one plan serves both directions"
  * (pkg/src/bfsht/alt.py:1-9).
@@ -63,5 +66,18 @@ typedef struct {
     int32_t ncols;       /* 0 when this parity half is absent                 */
     int32_t m;
 } bf_half;
+
+#ifdef __CUDACC__
+#define BF_HD __host__ __device__
+#else
+#define BF_HD
+#endif
+
+static inline BF_HD int64_t bf_tile_doubles(int R, int C) {
+    return (int64_t)((R + 3) / 4) * ((C + 3) / 4) * 16;
+}
+static inline BF_HD int64_t bf_tile_index(int r, int c, int C4) {
+    return ((int64_t)(r >> 2) * C4 + (c >> 2)) * 16 + (r & 3) * 4 + (c & 3);
+}
 
 #endif

@@ -58,6 +58,7 @@ struct bfsht_packed {
     int64_t payload_values = 0;
     int64_t n_bf = 0, n_lr = 0, n_dn = 0;
     int64_t n = 0, norders = 0;
+    int32_t yr = 0;   // row-major forward node array Yr[r][order][parity]
 };
 
 namespace {
@@ -265,7 +266,7 @@ struct Packer {
     }
     int64_t alloc_tile(int R, int C, const double *src, int64_t rs, int64_t cs) {
         int64_t at = P.n_tiles;
-        P.n_tiles += ((int64_t)R * C + 1) & ~int64_t(1);
+        P.n_tiles += bf_tile_doubles(R, C);
         jobs.push_back({at, R, C, src, rs, cs});
         return at;
     }
@@ -306,6 +307,9 @@ struct Packer {
         TaskBuild t;
         t.out = out;
         t.nout = nout;
+        // the engine consumes tasks as op streams: an empty task carries
+        // one no-op add so it still emits its (zero) outputs
+        if (ops.empty()) ops.push_back(mk(BF_OP_ADD, 0, 0, 0, 0, 0));
         for (auto &o : ops) t.cost += op_cost(o);
         t.ops = std::move(ops);
         stage(dir, s).push_back(std::move(t));
@@ -607,12 +611,19 @@ struct Packer {
         // group tasks: the last stage of each direction
         int last = 0;
         for (int d = 0; d < 2; ++d) last = std::max(last, (int)stages[d].size());
+        // forward results go to the row-major node array Yr[r][order][parity]
+        // (one contiguous 2 x norders run per node row), which the phi-DFT
+        // stage reads row pair by row pair; tasks write it with a stride
+        const int64_t yr_stride = 2 * (int64_t)M.norders;
+        if (yr_stride >= (1 << 23)) throw std::runtime_error("too many orders for the Yr stride");
+        P.yr = alloc_entries((int64_t)n * yr_stride);
         for (size_t hi = 0; hi < P.halves.size(); ++hi) {
             const bf_half &hf = P.halves[hi];
             if (hf.ncols <= 0) continue;
             for (size_t g = 0; g < fwd_groups[hi].size(); ++g)
-                add_task(0, last, hf.y + (int32_t)(g * BF_T),
-                         (int32_t)std::min<int64_t>(BF_T, n - (int64_t)g * BF_T),
+                add_task(0, last, P.yr + (int32_t)((int64_t)g * BF_T * yr_stride + (int64_t)hi),
+                         (int32_t)std::min<int64_t>(BF_T, n - (int64_t)g * BF_T) |
+                             (int32_t)(yr_stride << 8),
                          std::move(fwd_groups[hi][g]));
             for (size_t g = 0; g < inv_groups[hi].size(); ++g)
                 add_task(1, last, hf.x + (int32_t)(g * BF_T),
@@ -647,10 +658,12 @@ struct Packer {
         for (int64_t j = 0; j < nj; ++j) {
             const TileJob &t = jobs[j];
             double *dst = T + t.dst;
-            for (int c = 0; c < t.C; ++c)
-                for (int r = 0; r < t.R; ++r)
-                    dst[(int64_t)c * t.R + (r + c) % t.R] = t.src[r * t.rs + c * t.cs];
-            if (((int64_t)t.R * t.C) & 1) dst[(int64_t)t.R * t.C] = 0.0;
+            const int C4 = (t.C + 3) / 4, R4 = (t.R + 3) / 4;
+            std::memset(dst, 0, sizeof(double) * bf_tile_doubles(t.R, t.C));
+            for (int r = 0; r < t.R; ++r)
+                for (int c = 0; c < t.C; ++c)
+                    dst[bf_tile_index(r, c, C4)] = t.src[r * t.rs + c * t.cs];
+            (void)R4;
         }
     }
 };
@@ -688,7 +701,7 @@ extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]) {
     info[7] = (int64_t)p->stage_bounds[0].size() - 1;
     info[8] = (int64_t)p->stage_bounds[1].size() - 1;
     info[9] = p->payload_values;
-    info[10] = p->n_tiles;
+    info[10] = p->yr;
     info[11] = p->n_bf;
     info[12] = p->n_lr;
     info[13] = p->n_dn;

@@ -163,9 +163,9 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
         double2 go = make_double2(0.0, 0.0), ge = go;
         if (ho.ncols > 0)
-            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + rr) * BF_NRHS + sel);
+            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * BF_NRHS + sel);
         if (he.ncols > 0)
-            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + rr) * BF_NRHS + sel);
+            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)rr * he.x) * BF_NRHS + sel);
         const double2 t = tw[b];
         const int p = perm[b];
         buf[p] = cmul(make_double2(ge.x + go.x, ge.y + go.y), t);
@@ -216,13 +216,13 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
         sb = cmul(make_double2(sb.x * invL, sb.y * invL), t);
         const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
         if (ho.ncols > 0) {
-            double *e = arena + ((int64_t)ho.y + rr) * BF_NRHS;
+            double *e = arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * BF_NRHS;
             *reinterpret_cast<double2 *>(e + sel) =
                 make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
             if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
         }
         if (he.ncols > 0) {
-            double *e = arena + ((int64_t)he.y + rr) * BF_NRHS;
+            double *e = arena + ((int64_t)he.y + (int64_t)rr * he.x) * BF_NRHS;
             *reinterpret_cast<double2 *>(e + sel) =
                 make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
             if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
@@ -308,8 +308,8 @@ __global__ void orders_assemble_kernel(int n, const bf_half *__restrict__ halves
     if (r >= n) return;
     const bf_half ho = halves[2 * o], he = halves[2 * o + 1];
     double2 go = make_double2(0.0, 0.0), ge = go;
-    if (ho.ncols > 0) go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + r) * BF_NRHS);
-    if (he.ncols > 0) ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + r) * BF_NRHS);
+    if (ho.ncols > 0) go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)r * ho.x) * BF_NRHS);
+    if (he.ncols > 0) ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)r * he.x) * BF_NRHS);
     double2 *col = out + (int64_t)o * 2 * n;
     col[n + r] = make_double2(ge.x + go.x, ge.y + go.y);
     col[n - 1 - r] = make_double2(ge.x - go.x, ge.y - go.y);
@@ -445,7 +445,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
     sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
-        d, n, pl->halves, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
@@ -462,7 +462,7 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
     sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
-        d, n, pl->halves, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+        d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
         weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
@@ -488,7 +488,7 @@ int bf_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out, const 
         BF_CUDA(cudaGetLastError());
         int rc = bf_alt_apply(pl, dir, st);
         if (rc) return rc;
-        orders_assemble_kernel<<<g, 256, 0, st>>>(n, pl->halves, pl->arena,
+        orders_assemble_kernel<<<g, 256, 0, st>>>(n, pl->layout_fwd, pl->arena,
                                                   reinterpret_cast<double2 *>(out));
         BF_CUDA(cudaGetLastError());
     } else {

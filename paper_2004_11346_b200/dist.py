@@ -52,15 +52,18 @@ def _stream(torch):
 class ExchangePlan:
     """Host-side layout of the per-direction all-to-all (no device code).
 
-    send side: for each destination rank q (row pairs rows[q]), the node-half
-    entries of this rank's orders, order by order, odd then even half, rows
-    ascending — as arena entry indices (``send_idx``) and per-destination
-    counts.  receive side: the same chunks from every source rank s, laid
-    out so that entry (m, parity, r) sits at recv_halves[2m+parity].y +
-    (r - r0): the layout the DFT kernels read.
+    Chunks are row-major: the chunk for destination q holds, for each of
+    q's row pairs r (ascending), the 2 x len(orders) entries (order, parity)
+    of this rank — exactly one contiguous run of the forward node array
+    Yr[r][order][parity] per row (``send_idx``, a gather list).  For the
+    inverse the same positions map back to the m-major node halves the
+    inverse ALT reads (``scatter_idx``, -1 for absent halves).  On the
+    receive side the chunk from source s lands so that entry (m, parity, r)
+    sits at recv_layout[2m+parity].y + (r - r0) * recv_layout[2m+parity].x:
+    the addressing the DFT kernels take.
     """
 
-    def __init__(self, n, world, rank, halves):
+    def __init__(self, n, world, rank, halves, yr):
         self.n, self.world, self.rank = n, world, rank
         self.all_orders = lpt_orders(n, world)
         self.orders = self.all_orders[rank]
@@ -71,37 +74,30 @@ class ExchangePlan:
         if len(h) != 2 * len(self.orders) or \
                 list(h["m"][0::2]) != list(self.orders):
             raise ValueError("halves do not match this rank's orders")
-        send_idx, self.send_counts = [], []
+        w = 2 * len(self.orders)
+        ys = np.where(h["ncols"] > 0, h["y"], -1).astype(np.int64)
+        gather, scatter, self.send_counts = [], [], []
         for a, b in self.rows:
-            cnt = 0
-            for o in range(len(self.orders)):
-                for par in range(2):
-                    hf = h[2 * o + par]
-                    if hf["ncols"] == 0:
-                        continue
-                    send_idx.append(np.arange(hf["y"] + a, hf["y"] + b,
-                                              dtype=np.int32))
-                    cnt += b - a
-            self.send_counts.append(cnt)
-        self.send_idx = np.concatenate(send_idx) if send_idx \
-            else np.zeros(0, np.int32)
-        self.recv_halves = np.zeros(4 * n, dtype=HALF_DTYPE)
+            r = np.arange(a, b, dtype=np.int64)[:, None]
+            gather.append((yr + r * w + np.arange(w)[None, :]).ravel())
+            scatter.append(np.where(ys[None, :] >= 0, ys[None, :] + r, -1).ravel())
+            self.send_counts.append((b - a) * w)
+        self.send_idx = np.concatenate(gather).astype(np.int32)
+        self.scatter_idx = np.concatenate(scatter).astype(np.int32)
+        self.recv_layout = np.zeros(4 * n, dtype=HALF_DTYPE)
         self.recv_counts = []
         pos = 0
         for s in range(world):
-            cnt = 0
-            for m in self.all_orders[s]:
+            ws = 2 * len(self.all_orders[s])
+            for i, m in enumerate(self.all_orders[s]):
                 for par in range(2):
-                    hf = self.recv_halves[2 * m + par]
+                    hf = self.recv_layout[2 * m + par]
                     hf["m"] = m
-                    nc = half_cols(n, m, par)
-                    hf["ncols"] = nc
-                    if nc == 0:
-                        continue
-                    hf["y"] = pos
-                    pos += self.rc
-                    cnt += self.rc
-            self.recv_counts.append(cnt)
+                    hf["ncols"] = half_cols(n, m, par)
+                    hf["x"] = ws
+                    hf["y"] = pos + 2 * i + par
+            self.recv_counts.append(self.rc * ws)
+            pos += self.rc * ws
         self.recv_entries = pos
         offs, at = [], 0
         for m in self.orders:
@@ -236,14 +232,16 @@ class ShardedSht(_Common):
         lib = self.dp.lib
         self.lib = lib
         dev = self.dp.device
-        xp = ExchangePlan(n, world, rank, self.dp.packed.halves)
+        xp = ExchangePlan(n, world, rank, self.dp.packed.halves,
+                          int(self.dp.packed.info[10]))
         self.xp = xp
         self.all_orders, self.rows = xp.all_orders, xp.rows
         self.r0, self.rc = xp.r0, xp.rc
         self.send_idx = torch.from_numpy(xp.send_idx).to(dev)
+        self.scatter_idx = torch.from_numpy(xp.scatter_idx).to(dev)
         self.send_counts, self.recv_counts = xp.send_counts, xp.recv_counts
         self.recv_entries = xp.recv_entries
-        self.recv_halves = torch.from_numpy(xp.recv_halves.view(np.int32).copy()).to(dev)
+        self.recv_layout = torch.from_numpy(xp.recv_layout.view(np.int32).copy()).to(dev)
         self.sendbuf = torch.zeros((max(sum(xp.send_counts), 1), NRHS),
                                    dtype=torch.float64, device=dev)
         self.recvbuf = torch.zeros((max(xp.recv_entries, 1), NRHS),
@@ -274,17 +272,17 @@ class ShardedSht(_Common):
                                             self.send_idx.numel(), _ptr(self.sendbuf), st),
               "bfsht_gather_entries")
         self._a2a(self.recvbuf, self.sendbuf, self.recv_counts, self.send_counts)
-        check(lib, lib.bfsht_synth_rows(dp.handle, _ptr(self.recv_halves), _ptr(self.recvbuf),
+        check(lib, lib.bfsht_synth_rows(dp.handle, _ptr(self.recv_layout), _ptr(self.recvbuf),
                                         self.r0, self.rc, _ptr(grid), st), "bfsht_synth_rows")
 
     def inverse(self, grid, coeffs):
         lib, dp, st = self.lib, self.dp, _stream(self.torch)
-        check(lib, lib.bfsht_anal_rows(dp.handle, _ptr(self.recv_halves), _ptr(self.recvbuf),
+        check(lib, lib.bfsht_anal_rows(dp.handle, _ptr(self.recv_layout), _ptr(self.recvbuf),
                                        self.r0, self.rc, _ptr(grid), _ptr(self.weights), st),
               "bfsht_anal_rows")
         self._a2a(self.sendbuf, self.recvbuf, self.send_counts, self.recv_counts)
-        check(lib, lib.bfsht_scatter_entries(dp.handle, _ptr(self.send_idx),
-                                             self.send_idx.numel(), _ptr(self.sendbuf), st),
+        check(lib, lib.bfsht_scatter_entries(dp.handle, _ptr(self.scatter_idx),
+                                             self.scatter_idx.numel(), _ptr(self.sendbuf), st),
               "bfsht_scatter_entries")
         dp.alt_apply(INVERSE)
         check(lib, lib.bfsht_shard_unpack(dp.handle, _ptr(self.coeff_off), _ptr(coeffs), st),

@@ -57,7 +57,7 @@ NRHS = 4
 
 INFO_KEYS = ("tile_doubles", "ops", "idx", "maps", "tasks", "arena",
              "halves", "stages_fwd", "stages_inv", "payload_values",
-             "stored_doubles", "butterfly_blocks", "lowrank_blocks",
+             "yr", "butterfly_blocks", "lowrank_blocks",
              "dense_blocks", "n", "norders")
 
 

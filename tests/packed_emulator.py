@@ -13,10 +13,11 @@ F_GATHER, F_LANEMAP = 1, 2
 
 
 def tile_matrix(pk, off, R, C):
-    buf = pk.tiles[off:off + R * C]
+    """R x C tile stored as zero-padded 4x4 blocks (format.h)."""
+    c4 = (C + 3) // 4
     r = np.arange(R)[:, None]
     c = np.arange(C)[None, :]
-    return buf[c * R + (r + c) % R]
+    return pk.tiles[off + ((r >> 2) * c4 + (c >> 2)) * 16 + (r & 3) * 4 + (c & 3)]
 
 
 def run_direction(pk, arena, direction):
@@ -47,7 +48,9 @@ def run_direction(pk, arena, direction):
                         sl = lane - off
                     if 0 <= sl < width:
                         acc[lane] += res[sl]
-            arena[t["out"]:t["out"] + t["nout"]] = acc[:t["nout"]]
+            nout = int(t["nout"]) & 0xFF
+            stride = (int(t["nout"]) >> 8) or 1
+            arena[t["out"] + stride * np.arange(nout)] = acc[:nout]
 
 
 def alt_orders(pk, plans, direction, vectors, weights=None):
@@ -67,13 +70,15 @@ def alt_orders(pk, plans, direction, vectors, weights=None):
                 arena[hf["x"]:hf["x"] + hf["ncols"]] = np.stack(
                     [vals.real, vals.imag, 0 * vals.real, 0 * vals.real], 1)
         run_direction(pk, arena, 0)
+        yr, no = int(pk.info[10]), len(vectors)
         for o in range(len(vectors)):
             go = np.zeros(n, complex)
             ge = np.zeros(n, complex)
             for par, g in ((0, go), (1, ge)):
                 hf = h[2 * o + par]
                 if hf["ncols"]:
-                    e = arena[hf["y"]:hf["y"] + n]
+                    # forward results: row-major Yr[r][order][parity]
+                    e = arena[yr + np.arange(n) * 2 * no + 2 * o + par]
                     g[:] = e[:, 0] + 1j * e[:, 1]
             col = np.empty(2 * n, complex)
             col[n:] = ge + go

@@ -61,7 +61,7 @@ def _check_rank(rank, world):
     orders = lpt_orders(n, world)[rank]
     plans = plan_orders(n, orders, n0=8, processes=1, quadrature=q)
     pk = pack_plans(plans)
-    xp = ExchangePlan(n, world, rank, pk.halves)
+    xp = ExchangePlan(n, world, rank, pk.halves, int(pk.info[10]))
     flat = _flat(n, 11)
     full = plan_sht(n, n0=8)
     want_grid = OA.sht_forward(full.alt_plans, n, flat)
@@ -99,8 +99,8 @@ def _check_rank(rank, world):
             sel = 0 if m >= 0 else 2
             g = {}
             for par in range(2):
-                hf = xp.recv_halves[2 * abs(m) + par]
-                e = rv[hf["y"] + rr] if hf["ncols"] else np.zeros(4)
+                hf = xp.recv_layout[2 * abs(m) + par]
+                e = rv[hf["y"] + rr * hf["x"]] if hf["ncols"] else np.zeros(4)
                 g[par] = e[sel] + 1j * e[sel + 1]
             t = np.exp(1j * m * phi0)
             up[b] = (g[1] + g[0]) * t
@@ -124,15 +124,16 @@ def _check_rank(rank, world):
             t = np.exp(-1j * m * phi0)
             a, c = su[b] * t, sl[b] * t
             for par, v in ((0, w[n + r] * (a - c)), (1, w[n + r] * (a + c))):
-                hf = xp.recv_halves[2 * abs(m) + par]
+                hf = xp.recv_layout[2 * abs(m) + par]
                 if hf["ncols"]:
-                    ubuf[hf["y"] + rr, sel:sel + 2] = (v.real, v.imag)
+                    ubuf[hf["y"] + rr * hf["x"], sel:sel + 2] = (v.real, v.imag)
     back_send = torch.zeros((sum(xp.send_counts), 4), dtype=torch.float64)
     dist.all_to_all_single(back_send.view(-1), torch.from_numpy(ubuf).view(-1),
                            [c * 4 for c in xp.send_counts],
                            [c * 4 for c in xp.recv_counts])
     arena[:] = 0.0
-    arena[xp.send_idx] = back_send.numpy()
+    keep = xp.scatter_idx >= 0
+    arena[xp.scatter_idx[keep]] = back_send.numpy()[keep]
     EMU.run_direction(pk, arena, 1)
     for o, m in enumerate(orders):
         for sign in ((1, -1) if m else (1,)):
@@ -171,6 +172,6 @@ def test_exchange_plan_rejects_wrong_halves():
     from paper_2004_11346_b200.pack import pack_plans
     orders = lpt_orders(8, 2)[0]
     pk = pack_plans(plan_orders(8, orders, n0=8, processes=1))
-    ExchangePlan(8, 2, 0, pk.halves)
+    ExchangePlan(8, 2, 0, pk.halves, int(pk.info[10]))
     with pytest.raises(ValueError):
-        ExchangePlan(8, 2, 1, pk.halves)
+        ExchangePlan(8, 2, 1, pk.halves, int(pk.info[10]))
