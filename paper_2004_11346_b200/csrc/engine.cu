@@ -182,10 +182,7 @@ __device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) 
 // gather source of this lane for op r (-1: none); loaded one step early
 __device__ __forceinline__ int gather_src(const StageArgs &a, const Rec &r, int lane) {
     if (!r.valid || !(r.op.flags & BF_OPF_GATHER)) return -1;
-    if (r.op.kind == BF_OP_ADD) {
-        const int j = lane - r.op.off;
-        return (j >= 0 && j < r.op.R) ? __ldg(a.idx + r.op.in + j) : -1;
-    }
+    if (r.op.kind == BF_OP_ADD) return lane < r.op.R ? __ldg(a.idx + r.op.in + lane) : -1;
     const int nvec = (r.op.kind == BF_OP_TILE_N) ? r.op.C : r.op.R;
     return lane < nvec ? __ldg(a.idx + r.op.in + lane) : -1;
 }
@@ -208,8 +205,8 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s,
     int nvec = 0;
     int src = -1;
     if (op.kind == BF_OP_ADD) {
-        const int j = lane - op.off;
-        if (j >= 0 && j < op.R) src = gather ? gsrc : op.in + j;
+        // lane j < R fetches entry j (added into slot off + j by the consumer)
+        if (lane < op.R) src = gather ? gsrc : op.in + lane;
     } else {
         nvec = (op.kind == BF_OP_TILE_N) ? op.C : op.R;
         bytes = tile_bytes(op);
@@ -346,6 +343,17 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
     }
 }
 
+// result m-tiles 0..3 of an op onto accumulator m-tiles SH..SH+3
+template <int SH>
+__device__ __forceinline__ void place_tiles(double acc[8][2], const double e[4][2]) {
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+        if (SH + mt < 8) {
+            acc[SH + mt][0] += e[mt][0];
+            acc[SH + mt][1] += e[mt][1];
+        }
+}
+
 __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -382,10 +390,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
         q1 = advance(a, cur, lane);
     }
 
-    // task accumulator: acc[j] = slot 8j + lane/4, RHS 2(lane%4) .. +1
-    double acc[4][2];
+    // task accumulator: acc[j] = slot 8j + lane/4, RHS 2(lane%4) .. +1,
+    // 64 slots (dense group tasks use the first 32)
+    double acc[8][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
 
     while (seq_use < seq_issue) {
         const int s = seq_use % kStages;
@@ -395,12 +404,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
         const int4 tm = ring.tmeta[s];
         const double *V = ring.vec[s];
         if (op.kind == BF_OP_ADD) {
+            // entry j of the op (vec row j) adds into slot off + j
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int sl = 8 * j + g;
-                const int jj = sl - op.off;
+            for (int j = 0; j < 8; ++j) {
+                const int jj = 8 * j + g - op.off;
                 if (q < 2 && jj >= 0 && jj < op.R) {
-                    const double2 v = *reinterpret_cast<const double2 *>(V + sl * 4 + 2 * q);
+                    const double2 v = *reinterpret_cast<const double2 *>(V + jj * 4 + 2 * q);
                     acc[j][0] += v.x;
                     acc[j][1] += v.y;
                 }
@@ -411,33 +420,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
             const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
             if (!lanemap && (op.off & 7) == 0) {
                 // result m-tile mt lands on slot m-tile mt + off/8
-                // (explicit cases keep acc and e in registers)
+                // (one case per shift keeps acc and e in registers)
                 switch (op.off >> 3) {
-                    case 0:
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            acc[j][0] += e[j][0];
-                            acc[j][1] += e[j][1];
-                        }
-                        break;
-                    case 1:
-#pragma unroll
-                        for (int j = 1; j < 4; ++j) {
-                            acc[j][0] += e[j - 1][0];
-                            acc[j][1] += e[j - 1][1];
-                        }
-                        break;
-                    case 2:
-#pragma unroll
-                        for (int j = 2; j < 4; ++j) {
-                            acc[j][0] += e[j - 2][0];
-                            acc[j][1] += e[j - 2][1];
-                        }
-                        break;
-                    default:
-                        acc[3][0] += e[0][0];
-                        acc[3][1] += e[0][1];
-                        break;
+                    case 0: place_tiles<0>(acc, e); break;
+                    case 1: place_tiles<1>(acc, e); break;
+                    case 2: place_tiles<2>(acc, e); break;
+                    case 3: place_tiles<3>(acc, e); break;
+                    case 4: place_tiles<4>(acc, e); break;
+                    case 5: place_tiles<5>(acc, e); break;
+                    case 6: place_tiles<6>(acc, e); break;
+                    default: place_tiles<7>(acc, e); break;
                 }
             } else {
                 // general placement through the warp's scratch rows
@@ -451,9 +443,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
                             make_double2(e[mt][0], e[mt][1]);
                 __syncwarp();
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < 8; ++j) {
                     const int sl = 8 * j + g;
-                    const int src = lanemap ? (int)__ldg(a.maps + (int64_t)op.aux * BF_T + sl)
+                    const int src = lanemap ? (int)__ldg(a.maps + (int64_t)op.aux * BF_SLOTS + sl)
                                             : sl - op.off;
                     if (q < 2 && src >= 0 && src < width) {
                         const double2 v = *reinterpret_cast<const double2 *>(S + src * 4 + 2 * q);
@@ -468,7 +460,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
             const int nout = tm.y & 0xff;
             const int stride = (tm.y >> 8) ? (tm.y >> 8) : 1;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < 8; ++j) {
                 const int sl = 8 * j + g;
                 if (q < 2 && sl < nout) {
                     double *o = a.arena + ((int64_t)tm.x + (int64_t)sl * stride) * BF_NRHS + 2 * q;

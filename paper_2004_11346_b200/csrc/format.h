@@ -29,7 +29,8 @@
 #define BFSHT_FORMAT_H
 #include <stdint.h>
 
-#define BF_T 32          /* max tile edge / outputs per task */
+#define BF_T 32          /* max tile edge; dense group tasks write <= 32 entries */
+#define BF_SLOTS 64      /* max outputs per task (butterfly scatter tasks) */
 #define BF_NRHS 4        /* doubles per arena entry */
 
 enum bf_op_kind {

@@ -247,6 +247,7 @@ void segment_factor(int64_t nr, int64_t nc, int64_t nnz, const int64_t *gr,
 }
 
 struct Packer {
+    static constexpr int kMaxTaskOps = 48;   // longer group tasks are split
     bfsht_packed &P;
     const bfsht_manifest &M;
     std::vector<TileJob> jobs;
@@ -299,8 +300,8 @@ struct Packer {
         return (int32_t)at;
     }
     int32_t push_map(const int8_t *m) {
-        int64_t at = (int64_t)P.maps.size() / BF_T;
-        P.maps.insert(P.maps.end(), m, m + BF_T);
+        int64_t at = (int64_t)P.maps.size() / BF_SLOTS;
+        P.maps.insert(P.maps.end(), m, m + BF_SLOTS);
         return (int32_t)at;
     }
     void add_task(int dir, int s, int32_t out, int32_t nout, std::vector<bf_op> &&ops) {
@@ -406,15 +407,16 @@ struct Packer {
         }
     }
 
-    // column runs of a segment's dense columns cut at 32-chunks of its range
+    // column runs of a segment's dense columns: cut at the BF_SLOTS-position
+    // chunks of its range (one scatter task each) and at BF_T columns
     std::vector<std::pair<int64_t, int64_t>> tile_runs(const FactorSegs &fs, const Segment &s) {
         std::vector<std::pair<int64_t, int64_t>> runs;
         if (s.dcols.empty()) return runs;
         const int64_t a = fs.ranges[s.range].first;
         int64_t b = 0;
         for (int64_t j = 1; j <= (int64_t)s.dcols.size(); ++j) {
-            if (j == (int64_t)s.dcols.size() ||
-                (s.dcols[j] - a) / BF_T != (s.dcols[b] - a) / BF_T) {
+            if (j == (int64_t)s.dcols.size() || j - b == BF_T ||
+                (s.dcols[j] - a) / BF_SLOTS != (s.dcols[b] - a) / BF_SLOTS) {
                 runs.push_back({b, j});
                 b = j;
             }
@@ -430,17 +432,17 @@ struct Packer {
             if (fs.segs[si].range >= 0) by_range[fs.segs[si].range].push_back(si);
         for (size_t ri = 0; ri < fs.ranges.size(); ++ri) {
             const int64_t a = fs.ranges[ri].first, e = fs.ranges[ri].second;
-            for (int64_t q0 = a; q0 < e; q0 += BF_T) {
-                const int64_t qid = (q0 - a) / BF_T;
-                int nout = (int)std::min<int64_t>(BF_T, e - q0);
+            for (int64_t q0 = a; q0 < e; q0 += BF_SLOTS) {
+                const int64_t qid = (q0 - a) / BF_SLOTS;
+                int nout = (int)std::min<int64_t>(BF_SLOTS, e - q0);
                 std::vector<bf_op> ops;
                 for (size_t si : by_range[ri]) {
                     const Segment &s = fs.segs[si];
                     const auto runs = tile_runs(fs, s);
                     for (size_t q = 0; q < runs.size(); ++q) {
-                        if ((s.dcols[runs[q].first] - a) / BF_T != qid) continue;
+                        if ((s.dcols[runs[q].first] - a) / BF_SLOTS != qid) continue;
                         int C = (int)(runs[q].second - runs[q].first);
-                        int8_t lm[BF_T];
+                        int8_t lm[BF_SLOTS];
                         std::memset(lm, -1, sizeof(lm));
                         for (int c = 0; c < C; ++c)
                             lm[s.dcols[runs[q].first + c] - q0] = (int8_t)c;
@@ -452,14 +454,19 @@ struct Packer {
                                              BF_OPF_LANEMAP, mi));
                         }
                     }
-                    std::vector<int32_t> ln(nout, -1);
-                    bool any = false;
-                    for (auto &u : s.units) {
-                        if (u.second < q0 || u.second >= q0 + nout) continue;
-                        ln[u.second - q0] = in_vec + (int32_t)u.first;
-                        any = true;
+                    // identity entries: index adds of <= 32 lanes each
+                    for (int h0 = 0; h0 < nout; h0 += BF_T) {
+                        const int hn = std::min(BF_T, nout - h0);
+                        std::vector<int32_t> ln(hn, -1);
+                        bool any = false;
+                        for (auto &u : s.units) {
+                            if (u.second < q0 + h0 || u.second >= q0 + h0 + hn) continue;
+                            ln[u.second - q0 - h0] = in_vec + (int32_t)u.first;
+                            any = true;
+                        }
+                        if (any)
+                            ops.push_back(mk(BF_OP_ADD, 0, push_idx(ln), hn, 0, h0, BF_OPF_GATHER));
                     }
-                    if (any) ops.push_back(mk(BF_OP_ADD, 0, push_idx(ln), nout, 0, 0, BF_OPF_GATHER));
                 }
                 add_task(dir, st, out_vec + (int32_t)q0, nout, std::move(ops));
             }
@@ -630,6 +637,44 @@ struct Packer {
                          (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
                          std::move(inv_groups[hi][g]));
         }
+        // Long group tasks (e.g. the single column group of a half with a few
+        // columns, which collects every block of a tall thin matrix) would
+        // run for milliseconds on one warp while the rest of the GPU idles:
+        // split them into partial-sum tasks on scratch entries plus a
+        // combine task in an extra final stage (still a fixed summation
+        // order, so results stay bitwise reproducible).
+        for (int d = 0; d < 2; ++d) {
+            if (stages[d].empty()) continue;
+            std::vector<TaskBuild> &fin = stages[d].back();
+            std::vector<TaskBuild> combine;
+            std::vector<TaskBuild> keep_tasks;
+            for (auto &t : fin) {
+                if ((int)t.ops.size() <= kMaxTaskOps) {
+                    keep_tasks.push_back(std::move(t));
+                    continue;
+                }
+                const int nout = t.nout & 0xff;
+                TaskBuild c;
+                c.out = t.out;
+                c.nout = t.nout;
+                for (size_t b = 0; b < t.ops.size(); b += kMaxTaskOps) {
+                    const size_t e = std::min(t.ops.size(), b + kMaxTaskOps);
+                    TaskBuild part;
+                    part.out = alloc_entries(nout);
+                    part.nout = nout;
+                    part.ops.assign(t.ops.begin() + b, t.ops.begin() + e);
+                    for (auto &o : part.ops) part.cost += op_cost(o);
+                    for (int h0 = 0; h0 < nout; h0 += BF_T)
+                        c.ops.push_back(mk(BF_OP_ADD, 0, part.out + h0,
+                                           std::min(BF_T, nout - h0), 0, h0));
+                    keep_tasks.push_back(std::move(part));
+                }
+                for (auto &o : c.ops) c.cost += op_cost(o);
+                combine.push_back(std::move(c));
+            }
+            fin = std::move(keep_tasks);
+            if (!combine.empty()) stages[d].push_back(std::move(combine));
+        }
         // flatten: stages in order, tasks by descending cost
         for (int d = 0; d < 2; ++d) {
             P.stage_bounds[d].clear();
@@ -694,7 +739,7 @@ extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]) {
     info[0] = p->n_tiles;
     info[1] = (int64_t)p->ops.size();
     info[2] = (int64_t)p->idx.size();
-    info[3] = (int64_t)p->maps.size() / BF_T;
+    info[3] = (int64_t)p->maps.size() / BF_SLOTS;
     info[4] = (int64_t)p->tasks.size();
     info[5] = p->arena;
     info[6] = (int64_t)p->halves.size();

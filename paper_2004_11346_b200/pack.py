@@ -89,7 +89,7 @@ class PackedPlan:
         self.tiles = view(0, np.float64, s["tile_doubles"])
         self.ops = view(1, OP_DTYPE, s["ops"])
         self.idx = view(2, np.int32, s["idx"])
-        self.maps = view(3, np.int8, s["maps"] * 32)
+        self.maps = view(3, np.int8, s["maps"] * 64)
         self.tasks = view(4, TASK_DTYPE, s["tasks"])
         self.halves = view(5, HALF_DTYPE, s["halves"])
         self.stages_fwd = view(6, np.int64, s["stages_fwd"] + 1)

@@ -10,6 +10,7 @@ from paper_2004_11346_b200.pack import NRHS
 
 OP_N, OP_T, OP_ADD = 0, 1, 2
 F_GATHER, F_LANEMAP = 1, 2
+SLOTS = 64   # outputs per task (format.h BF_SLOTS)
 
 
 def tile_matrix(pk, off, R, C):
@@ -24,7 +25,7 @@ def run_direction(pk, arena, direction):
     bounds = pk.stages_fwd if direction == 0 else pk.stages_inv
     for s in range(len(bounds) - 1):
         for t in pk.tasks[bounds[s]:bounds[s + 1]]:
-            acc = np.zeros((32, NRHS))
+            acc = np.zeros((SLOTS, NRHS))
             for op in pk.ops[t["op_begin"]:t["op_begin"] + t["op_count"]]:
                 kind, R, C, off = int(op["kind"]), int(op["R"]), int(op["C"]), int(op["off"])
                 gather = bool(op["flags"] & F_GATHER)
@@ -41,13 +42,13 @@ def run_direction(pk, arena, direction):
                 v = arena[src]
                 res = a @ v if kind == OP_N else a.T @ v
                 width = res.shape[0]
-                for lane in range(32):
+                for slot in range(SLOTS):
                     if op["flags"] & F_LANEMAP:
-                        sl = int(pk.maps[int(op["aux"]) * 32 + lane])
+                        sl = int(pk.maps[int(op["aux"]) * SLOTS + slot])
                     else:
-                        sl = lane - off
+                        sl = slot - off
                     if 0 <= sl < width:
-                        acc[lane] += res[sl]
+                        acc[slot] += res[sl]
             nout = int(t["nout"]) & 0xFF
             stride = (int(t["nout"]) >> 8) or 1
             arena[t["out"] + stride * np.arange(nout)] = acc[:nout]
