@@ -52,8 +52,8 @@ __device__ __forceinline__ void butterfly(double2 *row, int base, int span, int 
 #pragma unroll
     for (int q = 0; q < P; ++q) {
         x[q] = row[base + q * span];
-        if (q > 0) x[q] = cmul(x[q], conjif(__ldg(W + q * k * tstep), inv));
-        root[q] = conjif(__ldg(W + q * rstep), inv);
+        if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
+        root[q] = conjif(W[q * rstep], inv);
     }
 #pragma unroll
     for (int s = 0; s < P; ++s) {
@@ -76,12 +76,12 @@ __device__ void butterfly_any(double2 *row, int base, int span, int k, int L, in
     const int rstep = L / P;
     for (int q = 0; q < P; ++q) {
         x[q] = row[base + q * span];
-        if (q > 0) x[q] = cmul(x[q], conjif(__ldg(W + q * k * tstep), inv));
+        if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
     }
     for (int s = 0; s < P; ++s) {
         double2 acc = x[0];
         for (int q = 1; q < P; ++q) {
-            double2 t = cmul(x[q], conjif(__ldg(W + ((q * s) % P) * rstep), inv));
+            double2 t = cmul(x[q], conjif(W[((q * s) % P) * rstep], inv));
             acc.x += t.x;
             acc.y += t.y;
         }
@@ -146,13 +146,21 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
-    double2 *scratch) {
+    double2 *scratch, bool w_smem) {
     // node-half entries of row pair r live at halves[.].y + (r - r_begin);
     // grid holds 2*r_count local rows: lower rows n-r_begin-r_count .. n-r_begin-1
     // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
     // r_begin = 0, r_count = n)
     const int L = d.L;
     double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    // twiddle table next to the rows in shared memory when it fits
+    const double2 *Wt = W;
+    if (use_smem && w_smem) {
+        double2 *ws = buf + 2 * L;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
+        __syncthreads();
+        Wt = ws;
+    }
     const int mtop = 2 * n - 1;
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
@@ -172,7 +180,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         buf[L + p] = cmul(make_double2(ge.x - go.x, ge.y - go.y), t);
     }
     __syncthreads();
-    dft_passes(buf, 2, d, W, true);
+    dft_passes(buf, 2, d, Wt, true);
     double2 *up = grid + (int64_t)(r_count + rr) * L;
     double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -189,9 +197,17 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
     const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
-    double2 *scratch) {
+    double2 *scratch, bool w_smem) {
     const int L = d.L;
     double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    // twiddle table next to the rows in shared memory when it fits
+    const double2 *Wt = W;
+    if (use_smem && w_smem) {
+        double2 *ws = buf + 2 * L;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
+        __syncthreads();
+        Wt = ws;
+    }
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
     const double2 *up = grid + (int64_t)(r_count + rr) * L;
@@ -202,7 +218,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
         buf[L + p] = lo[j];
     }
     __syncthreads();
-    dft_passes(buf, 2, d, W, false);
+    dft_passes(buf, 2, d, Wt, false);
     const double w = weights[n + r];
     const double invL = 1.0 / (double)L;
     const int mtop = 2 * n - 1;
@@ -368,6 +384,10 @@ DftDesc make_desc(const bfsht_plan *pl) {
 
 int dft_smem_bytes(int64_t L, int rows) { return (int)(rows * L * 16); }
 
+// two rows + the twiddle table when that fits the 227 KB opt-in limit
+bool dft_w_smem(int64_t L) { return 3 * L * 16 <= 227 * 1024; }
+int dft_pair_smem(int64_t L) { return dft_smem_bytes(L, dft_w_smem(L) ? 3 : 2); }
+
 }  // namespace
 
 int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
@@ -419,8 +439,9 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * L * rows));
         pl->dft_scratch_rows = rows;
     } else {
-        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
-        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+        const int pair = dft_pair_smem(L);
+        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
+        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
         BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
     }
     return 0;
@@ -444,10 +465,10 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
-    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch));
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -461,10 +482,10 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
-    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch));
+        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
@@ -530,11 +551,11 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(r_count, dft_grid_limit(pl));
-    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch));
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -548,11 +569,11 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(r_count, dft_grid_limit(pl));
-    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_smem_bytes(pl->dft_L, 2) : 0, st>>>(
+    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch));
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
