@@ -255,7 +255,8 @@ struct Packer {
     // tasks by direction and stage
     std::vector<std::vector<TaskBuild>> stages[2];
     // per half: group ops (fwd row groups over Y, inv col groups over X)
-    std::vector<std::vector<std::vector<bf_op>>> fwd_groups, inv_groups;
+    std::vector<std::vector<std::vector<bf_op>>> fwd_groups, inv_groups;  // dense tiles
+    std::vector<std::vector<std::vector<bf_op>>> fwd_other, inv_other;    // low-rank, butterfly
 
     Packer(bfsht_packed &p, const bfsht_manifest &m) : P(p), M(m) {}
 
@@ -352,7 +353,7 @@ struct Packer {
                 int64_t t = alloc_tile(R, K, v + (cc.first - b.c0) * r + k0, r, 1);
                 f1.push_back(mk(BF_OP_TILE_T, t, hf.x + (int32_t)cc.first, R, K, 0));
                 int gc = (int)(cc.first / BF_T);
-                inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_N, t, ti + (int32_t)k0, R, K,
+                inv_other[h_idx][gc].push_back(mk(BF_OP_TILE_N, t, ti + (int32_t)k0, R, K,
                                                    (int)(cc.first - (int64_t)gc * BF_T)));
             }
             for (auto rr : cuts(b.r0, b.r1)) {  // u s tiles: rows = block rows
@@ -360,7 +361,7 @@ struct Packer {
                 int64_t t = alloc_tile(R, K, u + (rr.first - b.r0) * r + k0, r, 1);
                 i1.push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, K, 0));
                 int g = (int)(rr.first / BF_T);
-                fwd_groups[h_idx][g].push_back(mk(BF_OP_TILE_N, t, tf + (int32_t)k0, R, K,
+                fwd_other[h_idx][g].push_back(mk(BF_OP_TILE_N, t, tf + (int32_t)k0, R, K,
                                                   (int)(rr.first - (int64_t)g * BF_T)));
             }
             add_task(0, 0, tf + (int32_t)k0, K, std::move(f1));
@@ -513,13 +514,13 @@ struct Packer {
         // block outputs into the group tasks
         for (auto rr : cuts(b.r0, b.r1)) {
             int g = (int)(rr.first / BF_T);
-            fwd_groups[h_idx][g].push_back(mk(BF_OP_ADD, 0, z[L] + (int32_t)(rr.first - b.r0),
+            fwd_other[h_idx][g].push_back(mk(BF_OP_ADD, 0, z[L] + (int32_t)(rr.first - b.r0),
                                               (int)(rr.second - rr.first), 0,
                                               (int)(rr.first - (int64_t)g * BF_T)));
         }
         for (auto cc : cuts(b.c0, b.c1)) {
             int gc = (int)(cc.first / BF_T);
-            inv_groups[h_idx][gc].push_back(mk(BF_OP_ADD, 0, zi[L] + (int32_t)(cc.first - b.c0),
+            inv_other[h_idx][gc].push_back(mk(BF_OP_ADD, 0, zi[L] + (int32_t)(cc.first - b.c0),
                                                (int)(cc.second - cc.first), 0,
                                                (int)(cc.first - (int64_t)gc * BF_T)));
         }
@@ -530,6 +531,8 @@ struct Packer {
         // halves and their arena vectors
         P.halves.resize((size_t)M.norders * 2);
         fwd_groups.resize(P.halves.size());
+        fwd_other.resize(P.halves.size());
+        inv_other.resize(P.halves.size());
         inv_groups.resize(P.halves.size());
         for (int o = 0; o < M.norders; ++o)
             for (int par = 0; par < 2; ++par) {
@@ -540,6 +543,8 @@ struct Packer {
                     hf.x = alloc_entries(hf.ncols);
                     hf.y = alloc_entries(n);
                     fwd_groups[o * 2 + par].resize((n + BF_T - 1) / BF_T);
+                    fwd_other[o * 2 + par].resize((n + BF_T - 1) / BF_T);
+                    inv_other[o * 2 + par].resize((hf.ncols + BF_T - 1) / BF_T);
                     inv_groups[o * 2 + par].resize((hf.ncols + BF_T - 1) / BF_T);
                 } else {
                     hf.x = hf.y = -1;
@@ -624,56 +629,88 @@ struct Packer {
         const int64_t yr_stride = 2 * (int64_t)M.norders;
         if (yr_stride >= (1 << 23)) throw std::runtime_error("too many orders for the Yr stride");
         P.yr = alloc_entries((int64_t)n * yr_stride);
+        // Group tasks.  The dense tiles of a group depend on nothing computed
+        // on the GPU, so they are dealt over the earlier stages (greedy by
+        // stage cost) where their big tiles keep HBM busy under the small,
+        // latency-bound butterfly and low-rank-core tasks; only the low-rank
+        // (u s) t / v t tiles and butterfly block outputs wait for the final
+        // stage, in a fix-up task that also adds the dense partial sums.  Long
+        // op lists (e.g. the single column group of a half with a few
+        // columns, which collects every block of a tall thin matrix) are
+        // chunked so no task runs for long on one warp.  Summation order is
+        // fixed by the packer, so results stay bitwise reproducible.
+        struct Pending {
+            int32_t out, nout;
+            std::vector<bf_op> dense, other;
+        };
+        std::vector<Pending> groups[2];
         for (size_t hi = 0; hi < P.halves.size(); ++hi) {
             const bf_half &hf = P.halves[hi];
             if (hf.ncols <= 0) continue;
             for (size_t g = 0; g < fwd_groups[hi].size(); ++g)
-                add_task(0, last, P.yr + (int32_t)((int64_t)g * BF_T * yr_stride + (int64_t)hi),
-                         (int32_t)std::min<int64_t>(BF_T, n - (int64_t)g * BF_T) |
-                             (int32_t)(yr_stride << 8),
-                         std::move(fwd_groups[hi][g]));
+                groups[0].push_back(
+                    {P.yr + (int32_t)((int64_t)g * BF_T * yr_stride + (int64_t)hi),
+                     (int32_t)std::min<int64_t>(BF_T, n - (int64_t)g * BF_T) |
+                         (int32_t)(yr_stride << 8),
+                     std::move(fwd_groups[hi][g]), std::move(fwd_other[hi][g])});
             for (size_t g = 0; g < inv_groups[hi].size(); ++g)
-                add_task(1, last, hf.x + (int32_t)(g * BF_T),
-                         (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
-                         std::move(inv_groups[hi][g]));
+                groups[1].push_back(
+                    {hf.x + (int32_t)(g * BF_T),
+                     (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
+                     std::move(inv_groups[hi][g]), std::move(inv_other[hi][g])});
         }
-        // Long group tasks (e.g. the single column group of a half with a few
-        // columns, which collects every block of a tall thin matrix) would
-        // run for milliseconds on one warp while the rest of the GPU idles:
-        // split them into partial-sum tasks on scratch entries plus a
-        // combine task in an extra final stage (still a fixed summation
-        // order, so results stay bitwise reproducible).
+        // a fix-up task must run in a later stage than the partials it adds
+        if (last == 0)
+            for (int d = 0; d < 2; ++d)
+                for (auto &gp : groups[d])
+                    if (!gp.other.empty() || gp.dense.size() > (size_t)kMaxTaskOps) last = 1;
+        for (int d = 0; d < 2; ++d) stage(d, last);
+        std::vector<double> load[2];
         for (int d = 0; d < 2; ++d) {
-            if (stages[d].empty()) continue;
-            std::vector<TaskBuild> &fin = stages[d].back();
-            std::vector<TaskBuild> combine;
-            std::vector<TaskBuild> keep_tasks;
-            for (auto &t : fin) {
-                if ((int)t.ops.size() <= kMaxTaskOps) {
-                    keep_tasks.push_back(std::move(t));
+            load[d].assign(stages[d].size(), 0.0);
+            for (size_t s = 0; s < stages[d].size(); ++s)
+                for (auto &t : stages[d][s]) load[d][s] += t.cost;
+        }
+        for (int d = 0; d < 2; ++d) {
+            std::vector<TaskBuild> early;   // dense parts, placed after sorting
+            for (auto &gp : groups[d]) {
+                const int nout = gp.nout & 0xff;
+                const size_t nd = gp.dense.size();
+                if (gp.other.empty() && nd <= (size_t)kMaxTaskOps && nd > 0) {
+                    TaskBuild t;
+                    t.out = gp.out;
+                    t.nout = gp.nout;
+                    for (auto &o : gp.dense) t.cost += op_cost(o);
+                    t.ops = std::move(gp.dense);
+                    early.push_back(std::move(t));
                     continue;
                 }
-                const int nout = t.nout & 0xff;
-                TaskBuild c;
-                c.out = t.out;
-                c.nout = t.nout;
-                for (size_t b = 0; b < t.ops.size(); b += kMaxTaskOps) {
-                    const size_t e = std::min(t.ops.size(), b + kMaxTaskOps);
+                std::vector<bf_op> fix;
+                for (size_t b = 0; b < nd; b += kMaxTaskOps) {
+                    const size_t e = std::min(nd, b + kMaxTaskOps);
                     TaskBuild part;
                     part.out = alloc_entries(nout);
                     part.nout = nout;
-                    part.ops.assign(t.ops.begin() + b, t.ops.begin() + e);
+                    part.ops.assign(gp.dense.begin() + b, gp.dense.begin() + e);
                     for (auto &o : part.ops) part.cost += op_cost(o);
                     for (int h0 = 0; h0 < nout; h0 += BF_T)
-                        c.ops.push_back(mk(BF_OP_ADD, 0, part.out + h0,
-                                           std::min(BF_T, nout - h0), 0, h0));
-                    keep_tasks.push_back(std::move(part));
+                        fix.push_back(mk(BF_OP_ADD, 0, part.out + h0, std::min(BF_T, nout - h0),
+                                         0, h0));
+                    early.push_back(std::move(part));
                 }
-                for (auto &o : c.ops) c.cost += op_cost(o);
-                combine.push_back(std::move(c));
+                fix.insert(fix.end(), gp.other.begin(), gp.other.end());
+                add_task(d, last, gp.out, gp.nout, std::move(fix));
             }
-            fin = std::move(keep_tasks);
-            if (!combine.empty()) stages[d].push_back(std::move(combine));
+            std::stable_sort(early.begin(), early.end(),
+                             [](const TaskBuild &x, const TaskBuild &y) { return x.cost > y.cost; });
+            const int nearly = last > 0 ? last : 1;
+            for (auto &t : early) {
+                int best = 0;
+                for (int s = 1; s < nearly; ++s)
+                    if (load[d][s] < load[d][best]) best = s;
+                load[d][best] += t.cost;
+                stage(d, best).push_back(std::move(t));
+            }
         }
         // flatten: stages in order, tasks by descending cost
         for (int d = 0; d < 2; ++d) {

@@ -43,28 +43,66 @@ __device__ __forceinline__ double2 conjif(double2 a, bool c) {
     return c ? make_double2(a.x, -a.y) : a;
 }
 
+// One radix-P pass over all butterflies of `nrows` rows (whole CTA).
+// Radix roots are loaded once per pass into registers.  Odd P uses the
+// conjugate-pair form: with a_j = x_j + x_{P-j}, b_j = x_j - x_{P-j},
+//   y_s, y_{P-s} = x_0 + sum_j a_j cos(2 pi js/P)  +/-  i sum_j b_j sin(..)
+// (signs per direction), about a quarter of the P^2 complex products of a
+// naive size-P DFT.
 template <int P>
-__device__ __forceinline__ void butterfly(double2 *row, int base, int span, int k, int L,
-                                          const double2 *__restrict__ W, bool inv) {
-    double2 x[P], root[P];
-    const int tstep = L / (span * P);
-    const int rstep = L / P;
+__device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int span,
+                                           const double2 *W, bool inv) {
+    double cr[P], ci[P];
 #pragma unroll
-    for (int q = 0; q < P; ++q) {
-        x[q] = row[base + q * span];
-        if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
-        root[q] = conjif(W[q * rstep], inv);
+    for (int t = 0; t < P; ++t) {
+        const double2 w = W[t * (L / P)];
+        cr[t] = w.x;
+        ci[t] = inv ? -w.y : w.y;
     }
+    const int nb = L / P;
+    const int tstep = L / (span * P);
+    for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
+        const int rw = t / nb, tt = t - rw * nb;
+        const int k = tt % span, g = tt / span;
+        double2 *row = buf + (int64_t)rw * L;
+        const int base = g * span * P + k;
+        double2 x[P];
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-        double2 acc = x[0];
-#pragma unroll
-        for (int q = 1; q < P; ++q) {
-            double2 t = cmul(x[q], root[(q * s) % P]);
-            acc.x += t.x;
-            acc.y += t.y;
+        for (int q = 0; q < P; ++q) {
+            x[q] = row[base + q * span];
+            if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
         }
-        row[base + s * span] = acc;
+        if (P == 2) {
+            row[base] = make_double2(x[0].x + x[1].x, x[0].y + x[1].y);
+            row[base + span] = make_double2(x[0].x - x[1].x, x[0].y - x[1].y);
+            continue;
+        }
+        constexpr int H = (P - 1) / 2;
+        double2 a[H + 1], bb[H + 1];
+        double2 y0 = x[0];
+#pragma unroll
+        for (int j = 1; j <= H; ++j) {
+            a[j] = make_double2(x[j].x + x[P - j].x, x[j].y + x[P - j].y);
+            bb[j] = make_double2(x[j].x - x[P - j].x, x[j].y - x[P - j].y);
+            y0.x += a[j].x;
+            y0.y += a[j].y;
+        }
+        row[base] = y0;
+#pragma unroll
+        for (int sidx = 1; sidx <= H; ++sidx) {
+            double2 re = x[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 1; j <= H; ++j) {
+                const int t = (j * sidx) % P;
+                re.x = fma(a[j].x, cr[t], re.x);
+                re.y = fma(a[j].y, cr[t], re.y);
+                im.x = fma(bb[j].x, ci[t], im.x);
+                im.y = fma(bb[j].y, ci[t], im.y);
+            }
+            // x_j w^{js} + x_{P-j} w^{-js} = a_j cr + i ci b_j
+            row[base + sidx * span] = make_double2(re.x - im.y, re.y + im.x);
+            row[base + (P - sidx) * span] = make_double2(re.x + im.y, re.y - im.x);
+        }
     }
 }
 
@@ -96,21 +134,20 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d,
     int span = 1;
     for (int ri = 0; ri < d.nrad; ++ri) {
         const int P = d.radix[ri];
-        const int nb = L / P;
-        for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
-            const int rw = t / nb, tt = t - rw * nb;
-            const int k = tt % span, g = tt / span;
-            double2 *row = buf + (int64_t)rw * L;
-            const int base = g * span * P + k;
-            switch (P) {
-                case 2: butterfly<2>(row, base, span, k, L, W, inv); break;
-                case 3: butterfly<3>(row, base, span, k, L, W, inv); break;
-                case 4: butterfly<4>(row, base, span, k, L, W, inv); break;
-                case 5: butterfly<5>(row, base, span, k, L, W, inv); break;
-                case 7: butterfly<7>(row, base, span, k, L, W, inv); break;
-                case 11: butterfly<11>(row, base, span, k, L, W, inv); break;
-                case 13: butterfly<13>(row, base, span, k, L, W, inv); break;
-                default: butterfly_any(row, base, span, k, L, P, W, inv); break;
+        switch (P) {
+            case 2: radix_pass<2>(buf, nrows, L, span, W, inv); break;
+            case 3: radix_pass<3>(buf, nrows, L, span, W, inv); break;
+            case 5: radix_pass<5>(buf, nrows, L, span, W, inv); break;
+            case 7: radix_pass<7>(buf, nrows, L, span, W, inv); break;
+            case 11: radix_pass<11>(buf, nrows, L, span, W, inv); break;
+            case 13: radix_pass<13>(buf, nrows, L, span, W, inv); break;
+            default: {
+                const int nb = L / P;
+                for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
+                    const int rw = t / nb, tt = t - rw * nb;
+                    const int k = tt % span, g = tt / span;
+                    butterfly_any(buf + (int64_t)rw * L, g * span * P + k, span, k, L, P, W, inv);
+                }
             }
         }
         __syncthreads();
