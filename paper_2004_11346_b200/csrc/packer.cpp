@@ -659,59 +659,35 @@ struct Packer {
                      (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
                      std::move(inv_groups[hi][g]), std::move(inv_other[hi][g])});
         }
-        // a fix-up task must run in a later stage than the partials it adds
-        if (last == 0)
-            for (int d = 0; d < 2; ++d)
-                for (auto &gp : groups[d])
-                    if (!gp.other.empty() || gp.dense.size() > (size_t)kMaxTaskOps) last = 1;
-        for (int d = 0; d < 2; ++d) stage(d, last);
-        std::vector<double> load[2];
+        // Measured on B200: interleaving the dense tiles into the (latency-
+        // bound) butterfly stages lowers their own streaming efficiency more
+        // than it hides the butterflies, so every group task runs in the
+        // final stage.  Tasks longer than kMaxTaskOps are chunked into
+        // partial sums on scratch entries, combined in one extra stage.
+        bool combine_stage = false;
         for (int d = 0; d < 2; ++d) {
-            load[d].assign(stages[d].size(), 0.0);
-            for (size_t s = 0; s < stages[d].size(); ++s)
-                for (auto &t : stages[d][s]) load[d][s] += t.cost;
-        }
-        for (int d = 0; d < 2; ++d) {
-            std::vector<TaskBuild> early;   // dense parts, placed after sorting
             for (auto &gp : groups[d]) {
-                const int nout = gp.nout & 0xff;
-                const size_t nd = gp.dense.size();
-                if (gp.other.empty() && nd <= (size_t)kMaxTaskOps && nd > 0) {
-                    TaskBuild t;
-                    t.out = gp.out;
-                    t.nout = gp.nout;
-                    for (auto &o : gp.dense) t.cost += op_cost(o);
-                    t.ops = std::move(gp.dense);
-                    early.push_back(std::move(t));
+                std::vector<bf_op> ops = std::move(gp.dense);
+                ops.insert(ops.end(), gp.other.begin(), gp.other.end());
+                if (ops.size() <= (size_t)kMaxTaskOps) {
+                    add_task(d, last, gp.out, gp.nout, std::move(ops));
                     continue;
                 }
-                std::vector<bf_op> fix;
-                for (size_t b = 0; b < nd; b += kMaxTaskOps) {
-                    const size_t e = std::min(nd, b + kMaxTaskOps);
-                    TaskBuild part;
-                    part.out = alloc_entries(nout);
-                    part.nout = nout;
-                    part.ops.assign(gp.dense.begin() + b, gp.dense.begin() + e);
-                    for (auto &o : part.ops) part.cost += op_cost(o);
+                const int nout = gp.nout & 0xff;
+                std::vector<bf_op> comb;
+                for (size_t b = 0; b < ops.size(); b += kMaxTaskOps) {
+                    const size_t e = std::min(ops.size(), b + kMaxTaskOps);
+                    const int32_t part = alloc_entries(nout);
+                    add_task(d, last, part, nout,
+                             std::vector<bf_op>(ops.begin() + b, ops.begin() + e));
                     for (int h0 = 0; h0 < nout; h0 += BF_T)
-                        fix.push_back(mk(BF_OP_ADD, 0, part.out + h0, std::min(BF_T, nout - h0),
-                                         0, h0));
-                    early.push_back(std::move(part));
+                        comb.push_back(mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
                 }
-                fix.insert(fix.end(), gp.other.begin(), gp.other.end());
-                add_task(d, last, gp.out, gp.nout, std::move(fix));
-            }
-            std::stable_sort(early.begin(), early.end(),
-                             [](const TaskBuild &x, const TaskBuild &y) { return x.cost > y.cost; });
-            const int nearly = last > 0 ? last : 1;
-            for (auto &t : early) {
-                int best = 0;
-                for (int s = 1; s < nearly; ++s)
-                    if (load[d][s] < load[d][best]) best = s;
-                load[d][best] += t.cost;
-                stage(d, best).push_back(std::move(t));
+                add_task(d, last + 1, gp.out, gp.nout, std::move(comb));
+                combine_stage = true;
             }
         }
+        (void)combine_stage;
         // flatten: stages in order, tasks by descending cost
         for (int d = 0; d < 2; ++d) {
             P.stage_bounds[d].clear();

@@ -201,6 +201,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     const int mtop = 2 * n - 1;
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
+#pragma unroll 4
     for (int b = threadIdx.x; b < L; b += blockDim.x) {
         const int m = b <= mtop ? b : b - L;
         const int am = m < 0 ? -m : m;
@@ -249,6 +250,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const int rr = r - r_begin;
     const double2 *up = grid + (int64_t)(r_count + rr) * L;
     const double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
+#pragma unroll 4
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
         const int p = perm[j];
         buf[p] = up[j];
