@@ -32,15 +32,21 @@
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kStages = 3;
+#ifndef BF_WARPS
+#define BF_WARPS 12
+#endif
+#ifndef BF_STAGES
+#define BF_STAGES 2
+#endif
+constexpr int kWarps = BF_WARPS;
+constexpr int kStages = BF_STAGES;
 constexpr int kTileDoubles = BF_T * BF_T;
 constexpr int kVecDoubles = BF_T * BF_NRHS;
 
 struct alignas(128) WarpRing {
     double tile[kStages][kTileDoubles];
     double vec[kStages][kVecDoubles];
-    double scratch[kVecDoubles];    // op result staging for remapped outputs
+    int8_t map[kStages][BF_SLOTS];  // lane map of the slot's op (prefetched)
     double zero[16];                // stands in for blocks past a tile edge
     bf_op meta[kStages];            // op descriptor of the slot's op
     int4 tmeta[kStages];            // task out, nout|stride<<8, last-op-of-task
@@ -132,20 +138,22 @@ struct Rec {
     int out, nout, last, valid;
 };
 
-// Walks the global task list as one flat op stream, one op per call.  The
-// next task is claimed one task ahead so that the claim (atomicAdd) and the
-// task-record load are off the critical path.
+// Walks the global task list as one flat op stream, one op per call.  Tasks
+// are claimed two ahead: the atomicAdd result of the claim after next sits
+// unread in lane 0 (raw) for a whole task, the next task's record is already
+// loaded, so neither the atomic nor the record load stalls the warp.
 struct Cursor {
     int base, n, i, out, nout;   // current task
-    int nt;                      // next claimed task id
+    int nt;                      // next task id (uniform)
     bf_task ntask;               // its record (valid when nt < ntasks)
+    int raw;                     // lane 0: claimed id of the task after next
 };
 
-__device__ __forceinline__ int claim(const StageArgs &a, int lane) {
-    int t = 0;
-    if (lane == 0) t = atomicAdd(a.counter, 1);
-    return __shfl_sync(0xffffffffu, t, 0);
+__device__ __forceinline__ int claim_raw(const StageArgs &a, int lane) {
+    return lane == 0 ? atomicAdd(a.counter, 1) : 0;
 }
+
+__device__ __forceinline__ int bcast(int raw) { return __shfl_sync(0xffffffffu, raw, 0); }
 
 __device__ __forceinline__ bf_task load_task(const StageArgs &a, int t) {
     const int4 v = __ldg(reinterpret_cast<const int4 *>(a.tasks + a.t0 + t));
@@ -167,8 +175,11 @@ __device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) 
         c.out = c.ntask.out;
         c.nout = c.ntask.nout;
         c.i = 0;
-        c.nt = claim(a, lane);
-        if (c.nt < a.ntasks) c.ntask = load_task(a, c.nt);
+        c.nt = bcast(c.raw);
+        if (c.nt < a.ntasks) {
+            c.ntask = load_task(a, c.nt);
+            c.raw = claim_raw(a, lane);
+        }
     }
     r.op = load_op(a.ops + c.base + c.i);
     r.out = c.out;
@@ -224,6 +235,8 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s,
         *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS]) = make_double2(0.0, 0.0);
         *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS + 2]) = make_double2(0.0, 0.0);
     }
+    if ((op.flags & BF_OPF_LANEMAP) && lane < BF_SLOTS / 16)
+        cp_async16(&ring.map[s][lane * 16], a.maps + (int64_t)op.aux * BF_SLOTS + lane * 16);
     cp_async_arrive(&ring.full[s]);
     if (lane == 0) {
         fence_proxy_async();
@@ -375,8 +388,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
     Cursor cur;
     cur.n = cur.i = 0;
     cur.base = cur.out = cur.nout = 0;
-    cur.nt = claim(a, lane);
-    if (cur.nt < a.ntasks) cur.ntask = load_task(a, cur.nt);
+    cur.nt = bcast(claim_raw(a, lane));
+    cur.raw = 0;
+    if (cur.nt < a.ntasks) {
+        cur.ntask = load_task(a, cur.nt);
+        cur.raw = claim_raw(a, lane);
+    }
 
     Rec q0 = advance(a, cur, lane);
     int g0 = gather_src(a, q0, lane);
@@ -433,7 +450,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
                 }
             } else {
                 // general placement through the warp's scratch rows
-                double *S = ring.scratch;
+                // the slot's input vector is dead once the product is formed:
+                // it doubles as the staging area for the placement
+                double *S = ring.vec[s];
+                __syncwarp();
                 const int width = (op.kind == BF_OP_TILE_N) ? op.R : op.C;
                 const int MT = (width + 7) >> 3;
 #pragma unroll
@@ -445,7 +465,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int sl = 8 * j + g;
-                    const int src = lanemap ? (int)__ldg(a.maps + (int64_t)op.aux * BF_SLOTS + sl)
+                    const int src = lanemap ? (int)ring.map[s][sl]
                                             : sl - op.off;
                     if (q < 2 && src >= 0 && src < width) {
                         const double2 v = *reinterpret_cast<const double2 *>(S + src * 4 + 2 * q);

@@ -155,18 +155,23 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d,
     }
 }
 
-__device__ __forceinline__ double2 *dft_buffer(double2 *scratch, int rows, int L, bool use_smem) {
+// SM is a template argument so that, once inlined, every row access is a
+// known shared-memory access (LDS/STS) rather than a generic one
+template <bool SM>
+__device__ __forceinline__ double2 *dft_buffer(double2 *scratch, int rows, int L) {
     extern __shared__ __align__(16) double2 dsm[];
-    return use_smem ? dsm : scratch + (int64_t)blockIdx.x * rows * L;
+    if (SM) return dsm;
+    return scratch + (int64_t)blockIdx.x * rows * L;
 }
 
 // ---- standalone batched DFT: rows of length L (numpy fft / L*ifft)
+template <bool SM>
 __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
     DftDesc d, const double2 *__restrict__ in, double2 *__restrict__ out, int64_t rows,
     const int *__restrict__ perm, const double2 *__restrict__ W, bool inv, bool use_smem,
     double2 *scratch) {
     const int L = d.L;
-    double2 *buf = dft_buffer(scratch, 1, L, use_smem);
+    double2 *buf = dft_buffer<SM>(scratch, 1, L);
     for (int64_t rw = blockIdx.x; rw < rows; rw += gridDim.x) {
         const double2 *src = in + rw * L;
         for (int j = threadIdx.x; j < L; j += blockDim.x) buf[perm[j]] = src[j];
@@ -179,6 +184,7 @@ __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
 }
 
 // ---- forward SHT: node halves -> assembled rows -> L*ifft -> grid rows
+template <bool SM>
 __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
@@ -189,10 +195,10 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
     // r_begin = 0, r_count = n)
     const int L = d.L;
-    double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    double2 *buf = dft_buffer<SM>(scratch, 2, L);
     // twiddle table next to the rows in shared memory when it fits
     const double2 *Wt = W;
-    if (use_smem && w_smem) {
+    if (SM && w_smem) {
         double2 *ws = buf + 2 * L;
         for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
         __syncthreads();
@@ -230,6 +236,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
 }
 
 // ---- inverse SHT: grid rows -> fft/L -> phase -> weighted fold -> node halves
+template <bool SM>
 __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, double *__restrict__ arena,
     const double2 *__restrict__ tw, const int *__restrict__ perm,
@@ -237,10 +244,10 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
     double2 *scratch, bool w_smem) {
     const int L = d.L;
-    double2 *buf = dft_buffer(scratch, 2, L, use_smem);
+    double2 *buf = dft_buffer<SM>(scratch, 2, L);
     // twiddle table next to the rows in shared memory when it fits
     const double2 *Wt = W;
-    if (use_smem && w_smem) {
+    if (SM && w_smem) {
         double2 *ws = buf + 2 * L;
         for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
         __syncthreads();
@@ -479,9 +486,9 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         pl->dft_scratch_rows = rows;
     } else {
         const int pair = dft_pair_smem(L);
-        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
-        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
-        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
+        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
+        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
     }
     return 0;
 }
@@ -504,7 +511,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
-    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
@@ -521,7 +528,7 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(n, dft_grid_limit(pl));
-    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
         weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
@@ -573,7 +580,7 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
     int grid = (int)(rows < 4096 ? rows : 4096);
     if (!sm) grid = (int)std::min<int64_t>(grid, pl->dft_scratch_rows);
     if (grid <= 0) return 0;
-    dft_rows_kernel<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) : 0, st>>>(
+    (sm ? dft_rows_kernel<true> : dft_rows_kernel<false>)<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) : 0, st>>>(
         make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
@@ -590,7 +597,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(r_count, dft_grid_limit(pl));
-    sht_synth_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
@@ -608,7 +615,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(r_count, dft_grid_limit(pl));
-    sht_anal_kernel<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
