@@ -79,8 +79,10 @@ int bfsht_pack_plan(const bfsht_manifest *man, int threads,
  * 5 arena entries, 6 halves, 7 stages fwd, 8 stages inv,
  * 9 payload values (sum of stored reference values), 10 arena entry of the
  * row-major forward node array Yr[r][order][parity], 11 butterfly blocks, 12 low-rank blocks, 13 dense blocks,
- * 14 half-size N, 15 number of order plans */
-int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]);
+ * 14 half-size N, 15 number of order plans, 16/17 index of the free
+ * (dependency-free dense) stage of the forward/inverse direction */
+#define BFSHT_INFO_LEN 24
+int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_LEN]);
 int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]);
 void bfsht_packed_free(bfsht_packed *p);
 
@@ -96,9 +98,13 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out);
  * dev[0..5] = tiles, ops, idx, maps, tasks, halves (bfsht_packed_arrays
  * order), dev[6] = vector arena (info[5] x 4 doubles); host[5..7] = host
  * copies of halves and the two stage-bound arrays. */
-int bfsht_plan_wrap(const int64_t info[16], const void *const host[8],
+int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
                     void *const dev[8], bfsht_plan **out);
 void bfsht_plan_free(bfsht_plan *pl);
+/* Scheduling knobs: overlap = run the dependency-free dense stage on its
+ * own SMs concurrently with the butterfly/low-rank chain (default 1);
+ * chain_ctas = SMs given to the chain (0 = default 40%). */
+int bfsht_plan_tune(bfsht_plan *pl, int overlap, int chain_ctas);
 /* Device pointer to the vector arena (info[5] entries x 4 doubles). */
 double *bfsht_plan_arena(bfsht_plan *pl);
 

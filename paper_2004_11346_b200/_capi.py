@@ -35,6 +35,8 @@ def declare(lib):
     lib.bfsht_sht_inverse.argtypes = [_P, _P, _P, _P, _P]
     lib.bfsht_dft_rows.restype = _I
     lib.bfsht_dft_rows.argtypes = [_I64, _I64, _I, _P, _P, _P]
+    lib.bfsht_plan_tune.restype = _I
+    lib.bfsht_plan_tune.argtypes = [_P, _I, _I]
     lib.bfsht_reset_launches.restype = _I
     lib.bfsht_reset_launches.argtypes = [_P]
     for name in ("bfsht_shard_pack", "bfsht_shard_unpack"):
@@ -53,7 +55,7 @@ def declare(lib):
 EXPORTS = (
     "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
     "bfsht_packed_free", "bfsht_last_error", "bfsht_plan_upload",
-    "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
+    "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena", "bfsht_plan_tune",
     "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_sht_forward",
     "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
     "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",

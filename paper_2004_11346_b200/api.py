@@ -26,7 +26,7 @@ import numpy as np
 
 from . import native
 from ._capi import check
-from .pack import NRHS, pack_plans
+from .pack import INFO_LEN, NRHS, pack_plans
 from .sht import ShtCoeffs, ShtGridValues
 
 FORWARD, INVERSE = 0, 1
@@ -103,7 +103,7 @@ class DevicePlan:
             self._host_halves = np.ascontiguousarray(pk.halves)
             self._sf = np.ascontiguousarray(pk.stages_fwd)
             self._si = np.ascontiguousarray(pk.stages_inv)
-            info = (ctypes.c_int64 * 16)(*[int(v) for v in pk.info])
+            info = (ctypes.c_int64 * INFO_LEN)(*[int(v) for v in pk.info])
             host = (ctypes.c_void_p * 8)()
             host[5] = self._host_halves.ctypes.data
             host[6] = self._sf.ctypes.data

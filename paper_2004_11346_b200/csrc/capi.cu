@@ -91,7 +91,7 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     const void *arr[8];
     bfsht_packed_arrays(p, arr);
     const size_t sz[6] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
-                          (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_T,
+                          (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
                           (size_t)pl->info[4] * sizeof(bf_task),
                           (size_t)pl->info[6] * sizeof(bf_half)};
     void *dev[6];
@@ -130,7 +130,7 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     return 0;
 }
 
-int bfsht_plan_wrap(const int64_t info[16], const void *const host[8], void *const dev[8],
+int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8], void *const dev[8],
                     bfsht_plan **out) {
     if (!info || !host || !dev || !out) {
         g_err = "null argument";
@@ -157,6 +157,9 @@ int bfsht_plan_wrap(const int64_t info[16], const void *const host[8], void *con
 
 void bfsht_plan_free(bfsht_plan *pl) {
     if (!pl) return;
+    if (pl->side) cudaStreamDestroy(pl->side);
+    if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
+    if (pl->ev_join) cudaEventDestroy(pl->ev_join);
     for (void *p : pl->owned) cudaFree(p);
     for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
                     (void *)pl->dft_scratch})
@@ -165,6 +168,13 @@ void bfsht_plan_free(bfsht_plan *pl) {
 }
 
 double *bfsht_plan_arena(bfsht_plan *pl) { return pl ? pl->arena : nullptr; }
+
+int bfsht_plan_tune(bfsht_plan *pl, int overlap, int chain_ctas) {
+    if (!pl) return -1;
+    pl->overlap = overlap != 0;
+    pl->chain_ctas = chain_ctas;
+    return 0;
+}
 
 int64_t bfsht_plan_launches(bfsht_plan *pl) { return pl ? pl->launches : -1; }
 
@@ -187,7 +197,8 @@ int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
         g_err = "stage out of range";
         return -1;
     }
-    return bf_run_stage(pl, b[stage], b[stage + 1], pl->counters + stage, (cudaStream_t)stream);
+    return bf_run_stage(pl, b[stage], b[stage + 1], pl->counters + stage, (cudaStream_t)stream,
+                        0);
 }
 
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,

@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
 
 static bool g_attr_set = false;
 
-int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st) {
+int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st,
+                 int max_ctas) {
     if (t1 <= t0) return 0;
     const size_t smem = sizeof(WarpRing) * kWarps;
     if (!g_attr_set) {
@@ -524,10 +525,58 @@ int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStrea
     a.counter = counter;
     BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     int64_t want = (a.ntasks + kWarps - 1) / kWarps;
-    int grid = (int)(want < pl->sm_count ? want : pl->sm_count);
+    const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;
+    int grid = (int)(want < cap ? want : cap);
     alt_stage_kernel<<<grid, kWarps * 32, smem, st>>>(a);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
+    return 0;
+}
+
+namespace {
+
+double stage_cost(const bfsht_plan *pl, int dir, int s) {
+    // proxy: tasks per stage weighted like the packer's LPT order; only
+    // used to split SMs between the chain and the free stage
+    const std::vector<int64_t> &b = pl->stages[dir];
+    return (double)(b[s + 1] - b[s]);
+}
+
+}  // namespace
+
+// The free stage (dense tiles, no device-side inputs) runs on a side stream
+// on its own SMs while the chain stages (butterfly factors, low-rank cores)
+// run on the caller's stream on the rest; the stages after it wait for both.
+// Each launch is persistent with one CTA per SM, so capping the two grids at
+// complementary CTA counts partitions the SMs between them.
+static int run_overlapped(bfsht_plan *pl, int dir, cudaStream_t st) {
+    const std::vector<int64_t> &b = pl->stages[dir];
+    const int nst = (int)b.size() - 1;
+    const int F = (int)pl->info[16 + dir];
+    if (!pl->side) {
+        BF_CUDA(cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking));
+        BF_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
+        BF_CUDA(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
+    }
+    // default split measured on B200 at N=1024 (scripts/tune_overlap.py):
+    // 40 of 148 SMs for the chain
+    const int chain_ctas = pl->chain_ctas > 0 ? pl->chain_ctas : (pl->sm_count * 27) / 100;
+    BF_CUDA(cudaEventRecord(pl->ev_fork, st));
+    BF_CUDA(cudaStreamWaitEvent(pl->side, pl->ev_fork, 0));
+    int rc = bf_run_stage(pl, b[F], b[F + 1], pl->counters + F, pl->side,
+                          pl->sm_count - chain_ctas);
+    if (rc) return rc;
+    BF_CUDA(cudaEventRecord(pl->ev_join, pl->side));
+    for (int s = 0; s < F; ++s) {
+        rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, chain_ctas);
+        if (rc) return rc;
+    }
+    BF_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
+    for (int s = F + 1; s < nst; ++s) {
+        rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, 0);
+        if (rc) return rc;
+    }
+    (void)stage_cost;
     return 0;
 }
 
@@ -538,8 +587,11 @@ int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t st) {
         bfsht_set_error("plan counters not allocated");
         return -3;
     }
+    const int F = (int)pl->info[16 + dir];
+    const bool overlap = pl->overlap && F > 0 && F < nst && b[F + 1] > b[F];
+    if (overlap) return run_overlapped(pl, dir, st);
     for (int s = 0; s < nst; ++s) {
-        int rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st);
+        int rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, 0);
         if (rc) return rc;
     }
     return 0;

@@ -10,7 +10,7 @@
 #include "format.h"
 
 struct bfsht_plan {
-    int64_t info[16];
+    int64_t info[BFSHT_INFO_LEN];
     const double *tiles = nullptr;
     const bf_op *ops = nullptr;
     const int32_t *idx = nullptr;
@@ -42,6 +42,11 @@ struct bfsht_plan {
     int64_t dft_scratch_rows = 0;
     int64_t launches = 0;
     int sm_count = 148;
+    // free-stage overlap (engine.cu run_overlapped)
+    bool overlap = true;
+    int chain_ctas = 0;               // 0: default split
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 void bfsht_set_error(const std::string &msg);
@@ -57,7 +62,7 @@ void bfsht_set_error(const std::string &msg);
 
 // engine.cu
 int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter,
-                 cudaStream_t s);
+                 cudaStream_t s, int max_ctas);
 int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
 // sht.cu
 int bf_dft_prepare(bfsht_plan *pl, int64_t L);

@@ -59,6 +59,7 @@ struct bfsht_packed {
     int64_t n_bf = 0, n_lr = 0, n_dn = 0;
     int64_t n = 0, norders = 0;
     int32_t yr = 0;   // row-major forward node array Yr[r][order][parity]
+    int32_t free_stage[2] = {-1, -1};   // dependency-free dense stage per direction
 };
 
 namespace {
@@ -659,35 +660,55 @@ struct Packer {
                      (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
                      std::move(inv_groups[hi][g]), std::move(inv_other[hi][g])});
         }
-        // Measured on B200: interleaving the dense tiles into the (latency-
-        // bound) butterfly stages lowers their own streaming efficiency more
-        // than it hides the butterflies, so every group task runs in the
-        // final stage.  Tasks longer than kMaxTaskOps are chunked into
-        // partial sums on scratch entries, combined in one extra stage.
-        bool combine_stage = false;
+        // Stage layout per direction:
+        //   0 .. last-1   chain: butterfly factors and low-rank cores
+        //   F = last      free: dense tiles only (no device-side inputs), run
+        //                 concurrently with the chain on its own SMs
+        //   X = last + 1  fix-up: dense partials + low-rank (u s) t / v t
+        //                 tiles + butterfly block outputs
+        //   C = last + 2  combine (only for fix-ups longer than kMaxTaskOps)
+        // Dense tiles hold ~85% of the bytes and stream at the HBM roofline;
+        // overlapping them with the latency-bound chain hides the chain.
+        // Long op lists (e.g. the single column group of a half with a few
+        // columns, which collects every block of a tall thin matrix) are
+        // chunked into partial sums so no task runs long on one warp.  The
+        // summation order is fixed here, so results are bitwise reproducible.
+        const int F = last, X = last + 1, C = last + 2;
         for (int d = 0; d < 2; ++d) {
+            stage(d, X);
             for (auto &gp : groups[d]) {
-                std::vector<bf_op> ops = std::move(gp.dense);
-                ops.insert(ops.end(), gp.other.begin(), gp.other.end());
-                if (ops.size() <= (size_t)kMaxTaskOps) {
-                    add_task(d, last, gp.out, gp.nout, std::move(ops));
+                const int nout = gp.nout & 0xff;
+                const size_t nd = gp.dense.size();
+                if (gp.other.empty() && nd <= (size_t)kMaxTaskOps) {
+                    add_task(d, nd ? F : X, gp.out, gp.nout, std::move(gp.dense));
                     continue;
                 }
-                const int nout = gp.nout & 0xff;
-                std::vector<bf_op> comb;
-                for (size_t b = 0; b < ops.size(); b += kMaxTaskOps) {
-                    const size_t e = std::min(ops.size(), b + kMaxTaskOps);
+                std::vector<bf_op> fix;
+                for (size_t b = 0; b < nd; b += kMaxTaskOps) {
+                    const size_t e = std::min(nd, b + kMaxTaskOps);
                     const int32_t part = alloc_entries(nout);
-                    add_task(d, last, part, nout,
-                             std::vector<bf_op>(ops.begin() + b, ops.begin() + e));
+                    add_task(d, F, part, nout,
+                             std::vector<bf_op>(gp.dense.begin() + b, gp.dense.begin() + e));
+                    for (int h0 = 0; h0 < nout; h0 += BF_T)
+                        fix.push_back(mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
+                }
+                fix.insert(fix.end(), gp.other.begin(), gp.other.end());
+                if (fix.size() <= (size_t)kMaxTaskOps) {
+                    add_task(d, X, gp.out, gp.nout, std::move(fix));
+                    continue;
+                }
+                std::vector<bf_op> comb;
+                for (size_t b = 0; b < fix.size(); b += kMaxTaskOps) {
+                    const size_t e = std::min(fix.size(), b + kMaxTaskOps);
+                    const int32_t part = alloc_entries(nout);
+                    add_task(d, X, part, nout, std::vector<bf_op>(fix.begin() + b, fix.begin() + e));
                     for (int h0 = 0; h0 < nout; h0 += BF_T)
                         comb.push_back(mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
                 }
-                add_task(d, last + 1, gp.out, gp.nout, std::move(comb));
-                combine_stage = true;
+                add_task(d, C, gp.out, gp.nout, std::move(comb));
             }
+            P.free_stage[d] = F;
         }
-        (void)combine_stage;
         // flatten: stages in order, tasks by descending cost
         for (int d = 0; d < 2; ++d) {
             P.stage_bounds[d].clear();
@@ -746,9 +767,11 @@ extern "C" int bfsht_pack_plan(const bfsht_manifest *man, int threads, bfsht_pac
     }
 }
 
-extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[16]) {
+extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_LEN]) {
     if (!p) return -1;
-    std::memset(info, 0, 16 * sizeof(int64_t));
+    std::memset(info, 0, BFSHT_INFO_LEN * sizeof(int64_t));
+    info[16] = p->free_stage[0];
+    info[17] = p->free_stage[1];
     info[0] = p->n_tiles;
     info[1] = (int64_t)p->ops.size();
     info[2] = (int64_t)p->idx.size();

@@ -510,7 +510,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     if (rc) return rc;
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
-    const int nblk = std::min(n, dft_grid_limit(pl));
+    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
@@ -527,7 +527,7 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     if (rc) return rc;
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
-    const int nblk = std::min(n, dft_grid_limit(pl));
+    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
@@ -596,7 +596,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     if (rc) return rc;
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
-    const int nblk = std::min(r_count, dft_grid_limit(pl));
+    const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
     (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
@@ -614,7 +614,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     if (rc) return rc;
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
-    const int nblk = std::min(r_count, dft_grid_limit(pl));
+    const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
     (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),

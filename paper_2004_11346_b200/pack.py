@@ -58,7 +58,8 @@ NRHS = 4
 INFO_KEYS = ("tile_doubles", "ops", "idx", "maps", "tasks", "arena",
              "halves", "stages_fwd", "stages_inv", "payload_values",
              "yr", "butterfly_blocks", "lowrank_blocks",
-             "dense_blocks", "n", "norders")
+             "dense_blocks", "n", "norders", "free_fwd", "free_inv")
+INFO_LEN = 24
 
 
 def _addr(a):
@@ -71,7 +72,7 @@ class PackedPlan:
     def __init__(self, handle, lib):
         self._h = handle
         self._lib = lib
-        info = (_I64 * 16)()
+        info = (_I64 * INFO_LEN)()
         lib.bfsht_packed_info(handle, info)
         self.info = np.array(list(info), dtype=np.int64)
         self.stats = dict(zip(INFO_KEYS, (int(v) for v in self.info)))
