@@ -29,6 +29,7 @@
 //    both, so a factor is stored once.  Depth-0 chains are dense blocks.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -673,8 +674,41 @@ struct Packer {
         // columns, which collects every block of a tall thin matrix) are
         // chunked into partial sums so no task runs long on one warp.  The
         // summation order is fixed here, so results are bitwise reproducible.
+        //
+        // Measured on B200 (N=1024, scripts/tune_overlap.py): the overlap
+        // saves ~65 us per direction but the extra fix-up stage of small
+        // tasks costs ~130 us, so by default every group task runs in the
+        // final stage (F = X); BFSHT_SPLIT_FREE=1 selects the split schedule.
+        const char *split_env = std::getenv("BFSHT_SPLIT_FREE");
+        const bool split = split_env && std::atoi(split_env) != 0;
+        if (!split) {
+            for (int d = 0; d < 2; ++d) {
+                for (auto &gp : groups[d]) {
+                    std::vector<bf_op> ops = std::move(gp.dense);
+                    ops.insert(ops.end(), gp.other.begin(), gp.other.end());
+                    if (ops.size() <= (size_t)kMaxTaskOps) {
+                        add_task(d, last, gp.out, gp.nout, std::move(ops));
+                        continue;
+                    }
+                    const int nout = gp.nout & 0xff;
+                    std::vector<bf_op> comb;
+                    for (size_t b = 0; b < ops.size(); b += kMaxTaskOps) {
+                        const size_t e = std::min(ops.size(), b + kMaxTaskOps);
+                        const int32_t part = alloc_entries(nout);
+                        add_task(d, last, part, nout,
+                                 std::vector<bf_op>(ops.begin() + b, ops.begin() + e));
+                        for (int h0 = 0; h0 < nout; h0 += BF_T)
+                            comb.push_back(
+                                mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
+                    }
+                    add_task(d, last + 1, gp.out, gp.nout, std::move(comb));
+                }
+            }
+            groups[0].clear();
+            groups[1].clear();
+        }
         const int F = last, X = last + 1, C = last + 2;
-        for (int d = 0; d < 2; ++d) {
+        for (int d = 0; d < 2 && split; ++d) {
             stage(d, X);
             for (auto &gp : groups[d]) {
                 const int nout = gp.nout & 0xff;
