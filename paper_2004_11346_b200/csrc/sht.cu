@@ -28,7 +28,10 @@
 namespace {
 
 constexpr int kMaxRadix = 24;
-constexpr int kDftThreads = 512;
+#ifndef BF_DFT_THREADS
+#define BF_DFT_THREADS 256
+#endif
+constexpr int kDftThreads = BF_DFT_THREADS;
 
 struct DftDesc {
     int L;
@@ -207,21 +210,44 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     const int mtop = 2 * n - 1;
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
-#pragma unroll 4
-    for (int b = threadIdx.x; b < L; b += blockDim.x) {
-        const int m = b <= mtop ? b : b - L;
-        const int am = m < 0 ? -m : m;
-        const int sel = m < 0 ? 2 : 0;
-        const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
-        double2 go = make_double2(0.0, 0.0), ge = go;
-        if (ho.ncols > 0)
-            go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * BF_NRHS + sel);
-        if (he.ncols > 0)
-            ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)rr * he.x) * BF_NRHS + sel);
-        const double2 t = tw[b];
-        const int p = perm[b];
-        buf[p] = cmul(make_double2(ge.x + go.x, ge.y + go.y), t);
-        buf[L + p] = cmul(make_double2(ge.x - go.x, ge.y - go.y), t);
+    // bins in batches of kBatch per thread: every load of a batch is issued
+    // before any is used (the layout lookup and the node-half loads are
+    // otherwise a chain of dependent DRAM latencies per bin)
+    constexpr int kBatch = 8;
+    for (int b0 = threadIdx.x; b0 < L; b0 += kBatch * blockDim.x) {
+        bf_half ho[kBatch], he[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int b = b0 + i * blockDim.x;
+            const int m = b < L ? (b <= mtop ? b : b - L) : 0;
+            const int am = m < 0 ? -m : m;
+            ho[i] = halves[2 * am];
+            he[i] = halves[2 * am + 1];
+        }
+        double2 go[kBatch], ge[kBatch], t[kBatch];
+        int p[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int b = b0 + i * blockDim.x;
+            const bool ok = b < L;
+            const int sel = (ok && b > mtop) ? 2 : 0;
+            go[i] = ge[i] = make_double2(0.0, 0.0);
+            if (ok && ho[i].ncols > 0)
+                go[i] = *reinterpret_cast<const double2 *>(
+                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * BF_NRHS + sel);
+            if (ok && he[i].ncols > 0)
+                ge[i] = *reinterpret_cast<const double2 *>(
+                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * BF_NRHS + sel);
+            t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
+            p[i] = ok ? perm[b] : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            if (b0 + i * blockDim.x < L) {
+                buf[p[i]] = cmul(make_double2(ge[i].x + go[i].x, ge[i].y + go[i].y), t[i]);
+                buf[L + p[i]] = cmul(make_double2(ge[i].x - go[i].x, ge[i].y - go[i].y), t[i]);
+            }
+        }
     }
     __syncthreads();
     dft_passes(buf, 2, d, Wt, true);
@@ -257,37 +283,65 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const int rr = r - r_begin;
     const double2 *up = grid + (int64_t)(r_count + rr) * L;
     const double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
-#pragma unroll 4
-    for (int j = threadIdx.x; j < L; j += blockDim.x) {
-        const int p = perm[j];
-        buf[p] = up[j];
-        buf[L + p] = lo[j];
+    constexpr int kBatch = 8;   // issue a batch of loads before using any
+    for (int j0 = threadIdx.x; j0 < L; j0 += kBatch * blockDim.x) {
+        double2 u[kBatch], v[kBatch];
+        int p[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int j = j0 + i * blockDim.x;
+            if (j < L) {
+                p[i] = perm[j];
+                u[i] = up[j];
+                v[i] = lo[j];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i)
+            if (j0 + i * blockDim.x < L) {
+                buf[p[i]] = u[i];
+                buf[L + p[i]] = v[i];
+            }
     }
     __syncthreads();
     dft_passes(buf, 2, d, Wt, false);
     const double w = weights[n + r];
     const double invL = 1.0 / (double)L;
     const int mtop = 2 * n - 1;
-    for (int b = threadIdx.x; b < L; b += blockDim.x) {
-        const int m = b <= mtop ? b : b - L;
-        const int am = m < 0 ? -m : m;
-        const int sel = m < 0 ? 2 : 0;
-        const double2 t = make_double2(tw[b].x, -tw[b].y);
-        double2 sa = buf[b], sb = buf[L + b];
-        sa = cmul(make_double2(sa.x * invL, sa.y * invL), t);
-        sb = cmul(make_double2(sb.x * invL, sb.y * invL), t);
-        const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
-        if (ho.ncols > 0) {
-            double *e = arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * BF_NRHS;
-            *reinterpret_cast<double2 *>(e + sel) =
-                make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
-            if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+    for (int b0 = threadIdx.x; b0 < L; b0 += kBatch * blockDim.x) {
+        bf_half ho[kBatch], he[kBatch];
+        double2 t[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int b = b0 + i * blockDim.x;
+            const int m = b < L ? (b <= mtop ? b : b - L) : 0;
+            const int am = m < 0 ? -m : m;
+            ho[i] = halves[2 * am];
+            he[i] = halves[2 * am + 1];
+            t[i] = b < L ? tw[b] : make_double2(0.0, 0.0);
         }
-        if (he.ncols > 0) {
-            double *e = arena + ((int64_t)he.y + (int64_t)rr * he.x) * BF_NRHS;
-            *reinterpret_cast<double2 *>(e + sel) =
-                make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
-            if (am == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int b = b0 + i * blockDim.x;
+            if (b >= L) continue;
+            const int m = b <= mtop ? b : b - L;
+            const int sel = m < 0 ? 2 : 0;
+            const double2 tc = make_double2(t[i].x, -t[i].y);
+            double2 sa = buf[b], sb = buf[L + b];
+            sa = cmul(make_double2(sa.x * invL, sa.y * invL), tc);
+            sb = cmul(make_double2(sb.x * invL, sb.y * invL), tc);
+            if (ho[i].ncols > 0) {
+                double *e = arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * BF_NRHS;
+                *reinterpret_cast<double2 *>(e + sel) =
+                    make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
+                if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+            }
+            if (he[i].ncols > 0) {
+                double *e = arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * BF_NRHS;
+                *reinterpret_cast<double2 *>(e + sel) =
+                    make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
+                if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+            }
         }
     }
     __syncthreads();
