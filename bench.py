@@ -11,8 +11,9 @@ n0 = 512.  A "step" = one sht_forward + one sht_inverse over that input.
 
 `value`: transforms/sec with plan and data resident in HBM (device-timed
 with CUDA events, max over ranks).  `e2e`: the same metric through the
-public host API (coefficients in host memory -> grid on host -> back),
-host<->device copies inside the timed region.  The payload (13.5 GB of fp64
+public host API (api.HostPipeline: pinned host coefficients -> host grid ->
+host coefficients for every step, host<->device copies inside the timed
+region, overlapped with other steps' transforms on copy streams).  The payload (13.5 GB of fp64
 factor values at N=1024) is far larger than the 126 MB L2, so every step
 streams it from HBM (no flush needed; stated in `config`).
 
@@ -366,6 +367,15 @@ def run_ours(args):
         t = torch.tensor([e2e["ms"]], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e["ms"] = float(t.item())
+    # the host output of the last timed step must be the input back
+    want = torch.from_numpy(np.ascontiguousarray(
+        runner.shard_coeffs(flat) if world > 1 else flat))
+    got = runner.last_e2e_output
+    t = torch.tensor([float(torch.linalg.norm(got - want)) ** 2,
+                      float(torch.linalg.norm(want)) ** 2], device=dev, dtype=torch.float64)
+    if world > 1:
+        torch.distributed.all_reduce(t)
+    e2e_rt = float((t[0] / t[1]).sqrt())
 
     check = None
     if args.check and world == 1:
@@ -398,7 +408,10 @@ def run_ours(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": 1e3 / e2e["ms"], "unit": UNIT,
-                    "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"]},
+                    "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
+                    "api": "api.HostPipeline (pinned host buffers; copies on "
+                           "their own streams overlap other steps' transforms)",
+                    "pipeline": e2e["pipelined"], "roundtrip_rel_l2": e2e_rt},
             "gpu_launches": launches,
             "clocks": clk,
             "roundtrip_rel_l2": rt,

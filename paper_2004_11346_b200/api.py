@@ -276,6 +276,129 @@ class ShtDevice:
     def inverse(self, grid, out=None, stream=None):
         return self.plan.sht_inverse(grid, out, stream)
 
+    def pipeline(self, depth=3):
+        """Host-buffer streaming handle (see HostPipeline)."""
+        n = self.n
+        return HostPipeline(
+            lambda c, g: self.plan.sht_forward(c, g),
+            lambda g, c: self.plan.sht_inverse(g, c),
+            self.plan.device, (4 * n * n,), (2 * n, 4 * n - 1), depth)
+
+
+class HostPipeline:
+    """Whole transforms on pinned HOST buffers, streamed.
+
+    ``forward(h_coeffs, h_grid)`` / ``inverse(h_grid, h_coeffs)`` enqueue
+    one transform each and return an event that completes when the host
+    output is written.  Every call copies its input host->device, runs the
+    transform, and copies the result device->host, on three streams:
+
+        h2d stream:     copy-in of job j+1 ...
+        compute stream: transform of job j (the plan's one work arena, so
+                        transforms are serialized in submission order)
+        d2h stream:     copy-out of job j-1 ...
+
+    so with several jobs in flight the PCIe traffic hides under the
+    transforms.  Dependencies are CUDA events only: device buffers rotate
+    through a ring of ``depth`` per shape and are reused after their last
+    reader/writer finished, and host buffers are tracked by address (a
+    copy-in waits for the copy-out that last wrote that host buffer, a
+    copy-out waits for the copy-in that last read it), so chaining
+    ``forward`` into ``inverse`` through the same host grid is safe without
+    a host synchronization.  Host buffers must be pinned torch tensors
+    (pageable memory would serialize the copies).
+    """
+
+    def __init__(self, run_forward, run_inverse, device, coeff_shape,
+                 grid_shape, depth=3):
+        torch = _torch()
+        self.torch = torch
+        self.run = {FORWARD: run_forward, INVERSE: run_inverse}
+        self.device = device
+        self.depth = int(depth)
+        if self.depth < 1:
+            raise ValueError("depth must be >= 1")
+        with torch.cuda.device(device):
+            self.s_in = torch.cuda.Stream(device)
+            self.s_run = torch.cuda.Stream(device)
+            self.s_out = torch.cuda.Stream(device)
+            shapes = {"c": tuple(coeff_shape), "g": tuple(grid_shape)}
+            self.pool = {k: [[torch.empty(s, dtype=torch.complex128, device=device),
+                              None] for _ in range(self.depth)]
+                         for k, s in shapes.items()}
+        self.next = {"c": 0, "g": 0}
+        self.shapes = shapes
+        self.host_write = {}   # host address -> event of the copy-out writing it
+        self.host_read = {}    # host address -> event of the copy-in reading it
+
+    def _slot(self, kind):
+        i = self.next[kind]
+        self.next[kind] = (i + 1) % self.depth
+        return self.pool[kind][i]
+
+    def _check(self, t, kind, name):
+        torch = self.torch
+        if not isinstance(t, torch.Tensor) or t.device.type != "cpu":
+            raise ValueError(f"{name} must be a host torch tensor")
+        if not t.is_pinned():
+            raise ValueError(f"{name} must be pinned (tensor.pin_memory())")
+        if t.dtype != torch.complex128 or not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous complex128")
+        if t.numel() != int(np.prod(self.shapes[kind])):
+            raise ValueError(f"{name} has {t.numel()} values, expected "
+                             f"{int(np.prod(self.shapes[kind]))}")
+
+    def _submit(self, direction, h_in, h_out):
+        torch = self.torch
+        kin, kout = ("c", "g") if direction == FORWARD else ("g", "c")
+        self._check(h_in, kin, "input")
+        self._check(h_out, kout, "output")
+        sin, sout = self._slot(kin), self._slot(kout)
+        ev = lambda: torch.cuda.Event()   # noqa: E731
+        # copy-in: after the last writer of the host buffer and the last
+        # user of the device slot
+        w = self.host_write.get(h_in.data_ptr())
+        if w is not None:
+            self.s_in.wait_event(w)
+        if sin[1] is not None:
+            self.s_in.wait_event(sin[1])
+        with torch.cuda.stream(self.s_in):
+            sin[0].view(-1).copy_(h_in.view(-1), non_blocking=True)
+            e_in = ev()
+            e_in.record(self.s_in)
+        self.host_read[h_in.data_ptr()] = e_in
+        # transform
+        self.s_run.wait_event(e_in)
+        if sout[1] is not None:
+            self.s_run.wait_event(sout[1])
+        with torch.cuda.stream(self.s_run):
+            self.run[direction](sin[0], sout[0])
+            e_run = ev()
+            e_run.record(self.s_run)
+        sin[1] = e_run
+        # copy-out: after the last reader of the host buffer
+        self.s_out.wait_event(e_run)
+        r = self.host_read.get(h_out.data_ptr())
+        if r is not None and h_out.data_ptr() != h_in.data_ptr():
+            self.s_out.wait_event(r)
+        with torch.cuda.stream(self.s_out):
+            h_out.view(-1).copy_(sout[0].view(-1), non_blocking=True)
+            e_out = ev()
+            e_out.record(self.s_out)
+        sout[1] = e_out
+        self.host_write[h_out.data_ptr()] = e_out
+        return e_out
+
+    def forward(self, h_coeffs, h_grid):
+        return self._submit(FORWARD, h_coeffs, h_grid)
+
+    def inverse(self, h_grid, h_coeffs):
+        return self._submit(INVERSE, h_grid, h_coeffs)
+
+    def synchronize(self):
+        for s in (self.s_in, self.s_run, self.s_out):
+            s.synchronize()
+
 
 def _sht_device(plan):
     dev = getattr(plan, "_b200_sht_device", None)

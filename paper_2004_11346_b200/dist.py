@@ -142,6 +142,63 @@ class _Common:
             out[name] = e0.elapsed_time(e1) / reps
         return out
 
+    def time_e2e(self, flat, steps, warmup, barrier, lag=2, depth=3):
+        """Host API end to end: pinned host coefficients -> host grid ->
+        host coefficients for every step, through api.HostPipeline (copies
+        on their own streams, overlapped with other steps' transforms).
+
+        Step j = forward(h_c[j]) into h_g[j], then inverse(h_g[j]) into
+        h_b[j]; forwards run `lag` steps ahead of inverses so the compute
+        stream has work while a grid travels device -> host -> device.
+        Every step's copies are inside the timed region (pipeline fill and
+        drain included)."""
+        import torch
+        from .api import HostPipeline
+        c, g, _ = self.make_buffers(flat)
+        coeff_shape, grid_shape = tuple(c.shape), tuple(g.shape)
+        host0 = torch.from_numpy(np.ascontiguousarray(
+            flat if not hasattr(self, "shard_coeffs") else self.shard_coeffs(flat)))
+        nbuf = lag + 2
+        h_c = [host0.clone().pin_memory() for _ in range(nbuf)]
+        h_g = [torch.empty(grid_shape, dtype=torch.complex128).pin_memory()
+               for _ in range(nbuf)]
+        h_b = [torch.empty(coeff_shape, dtype=torch.complex128).pin_memory()
+               for _ in range(nbuf)]
+        del c, g
+        pipe = HostPipeline(self.forward, self.inverse, self.dp.device,
+                            coeff_shape, grid_shape, depth)
+
+        def run(count):
+            for i in range(count + lag):
+                if i < count:
+                    k = i % nbuf
+                    pipe.forward(h_c[k], h_g[k])
+                j = i - lag
+                if j >= 0:
+                    k = j % nbuf
+                    pipe.inverse(h_g[k], h_b[k])
+
+        run(warmup)
+        pipe.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for s in (pipe.s_in, pipe.s_run, pipe.s_out):
+            s.wait_stream(torch.cuda.current_stream())
+        run(steps)
+        for s in (pipe.s_in, pipe.s_run, pipe.s_out):
+            torch.cuda.current_stream().wait_stream(s)
+        e1.record()
+        e1.synchronize()
+        barrier()
+        nb_c = h_c[0].numel() * 16
+        nb_g = h_g[0].numel() * 16
+        self.last_e2e_output = h_b[(steps - 1) % nbuf]
+        return {"ms": e0.elapsed_time(e1) / steps, "h2d": nb_c + nb_g,
+                "d2h": nb_g + nb_c, "pipelined": {"lag": lag, "depth": depth}}
+
 
 class SingleRunner(_Common):
     """Whole SHT on one GPU (plan holds every order)."""
@@ -171,45 +228,6 @@ class SingleRunner(_Common):
         self.inverse(grid, back)
         import torch
         return float(torch.linalg.norm(back - coeffs) / torch.linalg.norm(coeffs))
-
-    def time_e2e(self, flat, steps, warmup, barrier):
-        """Host API: numpy coefficients -> host grid -> host coefficients,
-        copies through pinned buffers inside the timed region."""
-        import torch
-        dev = self.dp.device
-        n = self.n
-        h_c = torch.from_numpy(flat).pin_memory()
-        h_g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128).pin_memory()
-        h_b = torch.empty_like(h_c).pin_memory()
-        d_c = torch.empty(h_c.shape, dtype=torch.complex128, device=dev)
-        d_g = torch.empty(h_g.shape, dtype=torch.complex128, device=dev)
-        d_b = torch.empty_like(d_c)
-
-        def step():
-            d_c.copy_(h_c, non_blocking=True)
-            self.dp.sht_forward(d_c, d_g)
-            h_g.copy_(d_g, non_blocking=True)
-            torch.cuda.current_stream().synchronize()   # grid is on the host
-            d_g.copy_(h_g, non_blocking=True)
-            self.dp.sht_inverse(d_g, d_b)
-            h_b.copy_(d_b, non_blocking=True)
-            torch.cuda.current_stream().synchronize()   # coefficients on host
-
-        for _ in range(warmup):
-            step()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            step()
-        e1.record()
-        barrier()
-        nb_c = h_c.numel() * 16
-        nb_g = h_g.numel() * 16
-        return {"ms": e0.elapsed_time(e1) / steps, "h2d": nb_c + nb_g,
-                "d2h": nb_g + nb_c}
-
 
 class ShardedSht(_Common):
     """Orders sharded over ranks, one NCCL all-to-all per direction.
@@ -312,41 +330,6 @@ class ShardedSht(_Common):
         t = torch.stack([num, den])
         self.dist.all_reduce(t, group=self.group)
         return float((t[0] / t[1]).sqrt())
-
-    def time_e2e(self, flat, steps, warmup, barrier):
-        torch = self.torch
-        dev = self.dp.device
-        h_c = torch.from_numpy(self.shard_coeffs(flat)).pin_memory()
-        n = self.n
-        h_g = torch.empty((2 * self.rc, 4 * n - 1), dtype=torch.complex128).pin_memory()
-        h_b = torch.empty_like(h_c).pin_memory()
-        d_c = torch.empty(h_c.shape, dtype=torch.complex128, device=dev)
-        d_g = torch.empty(h_g.shape, dtype=torch.complex128, device=dev)
-        d_b = torch.empty_like(d_c)
-
-        def step():
-            d_c.copy_(h_c, non_blocking=True)
-            self.forward(d_c, d_g)
-            h_g.copy_(d_g, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-            d_g.copy_(h_g, non_blocking=True)
-            self.inverse(d_g, d_b)
-            h_b.copy_(d_b, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
-
-        for _ in range(warmup):
-            step()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
-            step()
-        e1.record()
-        barrier()
-        return {"ms": e0.elapsed_time(e1) / steps,
-                "h2d": (h_c.numel() + h_g.numel()) * 16,
-                "d2h": (h_g.numel() + h_c.numel()) * 16}
 
 
 def _flat_offset(n, m):
