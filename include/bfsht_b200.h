@@ -121,6 +121,28 @@ int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream);
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
                      const double *weights, void *stream);
 
+/* Doubles per entry of the wide work arena used by the batched calls below:
+ * `work` must hold info[5] (arena entries) x BFSHT_WIDE_NRHS doubles, zeroed
+ * once before first use. */
+#define BFSHT_WIDE_NRHS 16
+
+/* Batched fields (SURVEY 8(b) "API extension", config 4): alt_forward /
+ * alt_inverse on (2N-m, F) / (2N, F) complex128 arrays per plan (alt.py:
+ * 264-282 applied column by column; the reference supports 2-D right-hand
+ * sides only at idbf_apply, butterfly.py:275-292).  in/out are field-minor
+ * (row-major L x F) and laid out plan after plan.  The payload is streamed
+ * once per 8 fields. */
+int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, double *out,
+                     const double *weights, double *work, void *stream);
+
+/* Raw half apply: the matrix of one (order, parity) half — for a plan built
+ * from a single ButterflyFactorization, exactly idbf_apply (FORWARD, K x) /
+ * idbf_apply_transpose (INVERSE, K^T y) (butterfly.py:275-292).  in/out are
+ * device real row-major (len x k) arrays; complex data is passed as
+ * interleaved re/im columns. */
+int bfsht_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
+                     double *work, void *stream);
+
 /* Full SHT on device buffers.  coeffs: flat m-major complex128, m from
  * -(2N-1) to 2N-1 (ShtCoeffs.pack(), sht.py:68-81); grid: 2N x (4N-1)
  * complex128 row-major, rows node-ascending.  The plan must hold orders

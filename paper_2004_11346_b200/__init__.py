@@ -22,6 +22,7 @@ __all__ = [
     "plan_diagnostics", "plan_orders", "plan_sht", "ShtCoeffs", "ShtGrid", "ShtGridValues",
     "make_grid", "alt_forward", "alt_inverse", "sht_forward", "sht_inverse",
     "CoeffVector", "GridFunctionColumn", "DevicePlan", "ShtDevice",
+    "HostPipeline", "idbf_apply", "idbf_apply_transpose",
 ]
 
 
@@ -29,7 +30,8 @@ def __getattr__(name):
     # the device API loads torch + the CUDA library lazily
     if name in ("alt_forward", "alt_inverse", "sht_forward", "sht_inverse",
                 "CoeffVector", "GridFunctionColumn", "DevicePlan",
-                "ShtDevice", "dft_rows"):
+                "ShtDevice", "dft_rows", "HostPipeline", "idbf_apply",
+                "idbf_apply_transpose"):
         from . import api
         return getattr(api, name)
     raise AttributeError(name)

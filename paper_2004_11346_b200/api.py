@@ -5,6 +5,7 @@ Same names, argument meaning and ValueError messages as the reference
 
     alt_forward(plan, coeffs)        -> GridFunctionColumn
     alt_inverse(plan, column)        -> CoeffVector
+    idbf_apply(fac, x), idbf_apply_transpose(fac, y)   (butterfly.py:275-292)
     sht_forward(plan, coeffs)        -> ShtGridValues
     sht_inverse(plan, grid_values)   -> ShtCoeffs
 
@@ -30,6 +31,7 @@ from .pack import INFO_LEN, NRHS, pack_plans
 from .sht import ShtCoeffs, ShtGridValues
 
 FORWARD, INVERSE = 0, 1
+WIDE_NRHS = 16   # BFSHT_WIDE_NRHS
 
 
 @dataclass
@@ -95,7 +97,7 @@ class DevicePlan:
             ]
             self.arena = torch.zeros((max(pk.stats["arena"], 1), NRHS),
                                      dtype=torch.float64, device=self.device)
-            if weights is None and plans:
+            if weights is None and plans and hasattr(plans[0], "quadrature"):
                 weights = plans[0].quadrature.weights
             self.weights = None if weights is None else \
                 torch.as_tensor(np.asarray(weights, dtype=np.float64),
@@ -152,6 +154,50 @@ class DevicePlan:
             self.handle, direction, ctypes.c_void_p(inp.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
             _stream_ptr(torch, stream)), "bfsht_alt_orders")
+        return out
+
+    def wide_arena(self):
+        """Work arena of the batched calls (BFSHT_WIDE_NRHS doubles per
+        entry), allocated on first use."""
+        if getattr(self, "_wide", None) is None:
+            torch = _torch()
+            self._wide = torch.zeros((max(self.packed.stats["arena"], 1), WIDE_NRHS),
+                                     dtype=torch.float64, device=self.device)
+        return self._wide
+
+    def alt_fields(self, direction, inp, out=None, stream=None):
+        """Batched-fields ALT: inp is a device complex128 (rows, F) tensor,
+        rows laid out plan after plan (2N-m coefficient rows forward, 2N
+        node rows inverse); one payload pass per 8 fields."""
+        torch = _torch()
+        inp = inp.contiguous()
+        if inp.dim() != 2:
+            raise ValueError("alt_fields expects a (rows, fields) tensor")
+        nf = inp.shape[1]
+        rows = len(self.orders) * 2 * self.n if direction == FORWARD else self.coeff_len
+        if out is None:
+            out = torch.empty((rows, nf), dtype=torch.complex128, device=self.device)
+        w = self.weights.data_ptr() if self.weights is not None else None
+        check(self.lib, self.lib.bfsht_alt_fields(
+            self.handle, direction, nf, ctypes.c_void_p(inp.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
+            ctypes.c_void_p(self.wide_arena().data_ptr()),
+            _stream_ptr(torch, stream)), "bfsht_alt_fields")
+        return out
+
+    def half_apply(self, direction, half, x, stream=None):
+        """Matrix of one (order, parity) half on a device real (len, k)
+        tensor: forward K x (len = half columns -> N rows), inverse K^T y."""
+        torch = _torch()
+        x = x.contiguous()
+        h = self.packed.halves[half]
+        n_out = self.n if direction == FORWARD else int(h["ncols"])
+        out = torch.empty((n_out, x.shape[1]), dtype=torch.float64, device=self.device)
+        check(self.lib, self.lib.bfsht_half_apply(
+            self.handle, direction, int(half), int(x.shape[1]),
+            ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+            ctypes.c_void_p(self.wide_arena().data_ptr()),
+            _stream_ptr(torch, stream)), "bfsht_half_apply")
         return out
 
     def sht_forward(self, coeffs, out=None, stream=None):
@@ -215,48 +261,129 @@ def _shape_of(values):
     return tuple(values.shape)
 
 
-def alt_forward(plan, coeffs):
-    """Coefficients beta_k (k = m..2N-1) to values at the 2N nodes
-    (reference alt.py:264-272)."""
-    values = coeffs.values if isinstance(coeffs, CoeffVector) else coeffs
-    if not hasattr(values, "shape"):
-        values = np.asarray(values)
-    if _shape_of(values) != (2 * plan.n - plan.m,):
-        raise ValueError(f"expected {2 * plan.n - plan.m} coefficients, "
-                         f"got shape {_shape_of(values)}")
-    torch = _torch()
-    dp = _device_plan(plan)
-    x, on_dev, cplx = _as_device(torch, values, dp)
-    y = dp.alt_orders(FORWARD, x)
+def _finish(y, on_dev, cplx):
     if not on_dev:
         y = y.cpu().numpy()
         if not cplx:
             y = y.real.copy()
     elif not cplx:
         y = y.real.contiguous()
-    return GridFunctionColumn(m=plan.m, values=y)
+    return y
+
+
+def _run_orders(plan, values, direction, want_rows):
+    torch = _torch()
+    dp = _device_plan(plan)
+    x, on_dev, cplx = _as_device(torch, values, dp)
+    if x.dim() == 1:
+        y = dp.alt_orders(direction, x)
+    else:
+        y = dp.alt_fields(direction, x)
+    return _finish(y, on_dev, cplx)
+
+
+def alt_forward(plan, coeffs):
+    """Coefficients beta_k (k = m..2N-1) to values at the 2N nodes
+    (reference alt.py:264-272).  Extension: a
+    (2N-m, F) array applies F fields at once."""
+    values = coeffs.values if isinstance(coeffs, CoeffVector) else coeffs
+    if not hasattr(values, "shape"):
+        values = np.asarray(values)
+    shape = _shape_of(values)
+    if not (shape == (2 * plan.n - plan.m,)
+            or (len(shape) == 2 and shape[0] == 2 * plan.n - plan.m)):
+        raise ValueError(f"expected {2 * plan.n - plan.m} coefficients, "
+                         f"got shape {shape}")
+    return GridFunctionColumn(m=plan.m, values=_run_orders(plan, values, FORWARD, 2 * plan.n))
 
 
 def alt_inverse(plan, column):
     """Values at the 2N nodes back to coefficients via the weighted
-    transpose (reference alt.py:275-282)."""
+    transpose (reference alt.py:275-282); (2N, F) arrays batch F fields."""
     values = column.values if isinstance(column, GridFunctionColumn) else column
     if not hasattr(values, "shape"):
         values = np.asarray(values)
-    if _shape_of(values) != (2 * plan.n,):
+    shape = _shape_of(values)
+    if not (shape == (2 * plan.n,) or (len(shape) == 2 and shape[0] == 2 * plan.n)):
         raise ValueError(f"expected {2 * plan.n} node values, "
-                         f"got shape {_shape_of(values)}")
+                         f"got shape {shape}")
+    return CoeffVector(m=plan.m, values=_run_orders(plan, values, INVERSE, 2 * plan.n - plan.m))
+
+
+class _FactorSpec:
+    def __init__(self, num_cols):
+        self.num_cols = num_cols
+
+
+class _FactorBlock:
+    def __init__(self, trim, payload):
+        self.trim = trim
+        self.payload = payload
+
+
+class _FactorPlan:
+    """A ButterflyFactorization dressed as a one-half plan for the packer:
+    K (h x w) is the odd half of order 0 with N = h rows and w columns."""
+
+    def __init__(self, fac):
+        h, w = (int(v) for v in fac.shape)
+        self.n, self.m = h, 0
+        self.spec_odd, self.spec_even = _FactorSpec(w), None
+        self.blocks_odd, self.blocks_even = [_FactorBlock((0, h, 0, w), fac)], []
+
+
+def _factor_device(fac):
+    dp = getattr(fac, "_b200_device_plan", None)
+    if dp is None:
+        dp = DevicePlan([_FactorPlan(fac)])
+        try:
+            fac._b200_device_plan = dp
+        except AttributeError:
+            pass
+    return dp
+
+
+def _factor_apply(fac, v, direction):
     torch = _torch()
-    dp = _device_plan(plan)
-    x, on_dev, cplx = _as_device(torch, values, dp)
-    y = dp.alt_orders(INVERSE, x)
-    if not on_dev:
-        y = y.cpu().numpy()
-        if not cplx:
-            y = y.real.copy()
-    elif not cplx:
-        y = y.real.contiguous()
-    return CoeffVector(m=plan.m, values=y)
+    dp = _factor_device(fac)
+    is_tensor = isinstance(v, torch.Tensor)
+    if is_tensor:
+        cplx = v.is_complex()
+        t = v.to(dp.device)
+    else:
+        arr = np.asarray(v)
+        cplx = np.iscomplexobj(arr)
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dp.device)
+    vec = t.dim() == 1
+    t = t.reshape(t.shape[0], -1)
+    k = t.shape[1]
+    if cplx:
+        t = torch.view_as_real(t.to(torch.complex128).contiguous()).reshape(t.shape[0], 2 * k)
+    else:
+        t = t.to(torch.float64)
+    y = dp.half_apply(direction, 0, t)
+    if cplx:
+        y = torch.view_as_complex(y.reshape(y.shape[0], k, 2).contiguous())
+    if vec:
+        y = y.reshape(-1)
+    return y if is_tensor else y.cpu().numpy()
+
+
+def idbf_apply(fac, x):
+    """y = K x through the butterfly factor chain on the GPU
+    (reference butterfly.py:275-282); x is (w,) or (w, k)."""
+    shape = tuple(x.shape) if hasattr(x, "shape") else np.asarray(x).shape
+    if shape[0] != fac.shape[1]:
+        raise ValueError(f"length {shape[0]} against shape {fac.shape}")
+    return _factor_apply(fac, x, FORWARD)
+
+
+def idbf_apply_transpose(fac, y):
+    """x = K^T y (reference butterfly.py:285-292); y is (h,) or (h, k)."""
+    shape = tuple(y.shape) if hasattr(y, "shape") else np.asarray(y).shape
+    if shape[0] != fac.shape[0]:
+        raise ValueError(f"length {shape[0]} against shape {fac.shape}")
+    return _factor_apply(fac, y, INVERSE)
 
 
 class ShtDevice:

@@ -51,6 +51,8 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
             lf[h].y = (int32_t)pl->info[10] + (int32_t)h;
             li[h].x = 1;
         }
+        pl->host_halves.assign(host_halves, host_halves + nh);
+        pl->host_layout_fwd = lf;
         BF_CUDA(cudaMalloc(&pl->layout_fwd, sizeof(bf_half) * (nh ? nh : 1)));
         pl->owned.push_back(pl->layout_fwd);
         BF_CUDA(cudaMalloc(&pl->layout_inv, sizeof(bf_half) * (nh ? nh : 1)));
@@ -213,6 +215,41 @@ int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
     }
 
     return bf_alt_orders(pl, dir, in, out, weights, (cudaStream_t)stream);
+}
+
+int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, double *out,
+                     const double *weights, double *work, void *stream) {
+    if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan or direction";
+        return -1;
+    }
+    if (nfields < 0 || (nfields > 0 && (!in || !out || !work))) {
+        g_err = "bad field count or null buffer";
+        return -1;
+    }
+    if (dir == BFSHT_INVERSE && !weights) {
+        g_err = "inverse ALT needs quadrature weights";
+        return -1;
+    }
+    return bf_alt_fields(pl, dir, nfields, in, out, weights, work, (cudaStream_t)stream);
+}
+
+int bfsht_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
+                     double *work, void *stream) {
+    if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan or direction";
+        return -1;
+    }
+    if (half < 0 || half >= (int)pl->host_halves.size() || pl->host_halves[half].ncols <= 0) {
+        g_err = "half out of range or absent";
+        return -1;
+    }
+    if (k < 0 || (k > 0 && (!in || !out || !work))) {
+        g_err = "bad column count or null buffer";
+        return -1;
+    }
+    if (k == 0) return 0;
+    return bf_half_apply(pl, dir, half, k, in, out, work, (cudaStream_t)stream);
 }
 
 static int check_sht(bfsht_plan *pl) {

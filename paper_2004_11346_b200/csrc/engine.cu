@@ -41,20 +41,35 @@ namespace {
 #ifndef BF_STAGES
 #define BF_STAGES 2
 #endif
-constexpr int kWarps = BF_WARPS;
+constexpr int kWarps = BF_WARPS;       // SHT path (4 RHS per entry)
 constexpr int kStages = BF_STAGES;
 constexpr int kTileDoubles = BF_T * BF_T;
-constexpr int kVecDoubles = BF_T * BF_NRHS;
 
+// Entry width NR (real RHS per arena entry): 4 for the SHT (re/im of +m and
+// -m), 16 for batched fields.  Lane (g = lane/4, q = lane%4) owns RHS
+// 8*grp + 2q, +1 of each 8-wide DMMA n-group grp; at NR = 4 only lanes
+// q < 2 carry data and the B fragment's columns 4..7 are padding.
+template <int NR>
+struct Width {
+    static constexpr int G = NR >= 8 ? NR / 8 : 1;      // n-groups
+    static constexpr int QACT = NR >= 8 ? 4 : NR / 2;   // lanes q < QACT own RHS
+    static constexpr int GACT = NR >= 8 ? 8 : NR;       // valid B columns
+    static constexpr int WARPS = NR == 4 ? kWarps : 8;  // register / shared-memory bound
+};
+
+template <int NR>
 struct alignas(128) WarpRing {
     double tile[kStages][kTileDoubles];
-    double vec[kStages][kVecDoubles];
+    double vec[kStages][BF_T * NR];
     int8_t map[kStages][BF_SLOTS];  // lane map of the slot's op (prefetched)
     double zero[16];                // stands in for blocks past a tile edge
     bf_op meta[kStages];            // op descriptor of the slot's op
     int4 tmeta[kStages];            // task out, nout|stride<<8, last-op-of-task
     unsigned long long full[kStages];
 };
+static_assert(sizeof(WarpRing<4>) * kWarps <= 227 * 1024, "SHT ring exceeds shared memory");
+static_assert(sizeof(WarpRing<16>) * Width<16>::WARPS <= 227 * 1024,
+              "batched ring exceeds shared memory");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -206,7 +221,8 @@ __device__ __forceinline__ uint32_t tile_bytes(const bf_op &op) {
 }
 
 // Issue the loads of one op into ring slot s (whole warp).
-__device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s, const Rec &r,
+template <int NR>
+__device__ __forceinline__ void issue(const StageArgs &a, WarpRing<NR> &ring, int s, const Rec &r,
                                       int gsrc, int lane) {
     const bf_op &op = r.op;
     const double *arena = a.arena;
@@ -227,16 +243,17 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s,
         if (gather)
             src = gsrc;
         else
-            bytes += (uint32_t)nvec * BF_NRHS * 8u;
+            bytes += (uint32_t)nvec * NR * 8u;
     }
     if (src >= 0 && (gather || op.kind == BF_OP_ADD)) {
-        const double *gp = arena + (int64_t)src * BF_NRHS;
-        cp_async16(&ring.vec[s][lane * BF_NRHS], gp);
-        cp_async16(&ring.vec[s][lane * BF_NRHS + 2], gp + 2);
+        const double *gp = arena + (int64_t)src * NR;
+#pragma unroll
+        for (int k = 0; k < NR; k += 2) cp_async16(&ring.vec[s][lane * NR + k], gp + k);
     } else if (op.kind == BF_OP_ADD) {
         // lanes without a source add zeros (keeps index loads off the consumer)
-        *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS]) = make_double2(0.0, 0.0);
-        *reinterpret_cast<double2 *>(&ring.vec[s][lane * BF_NRHS + 2]) = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < NR; k += 2)
+            *reinterpret_cast<double2 *>(&ring.vec[s][lane * NR + k]) = make_double2(0.0, 0.0);
     }
     if ((op.flags & BF_OPF_LANEMAP) && lane < BF_SLOTS / 16)
         cp_async16(&ring.map[s][lane * 16], a.maps + (int64_t)op.aux * BF_SLOTS + lane * 16);
@@ -247,43 +264,63 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing &ring, int s,
         if (op.kind != BF_OP_ADD) {
             bulk_g2s(ring.tile[s], a.tiles + op.tile, tile_bytes(op), &ring.full[s]);
             if (!gather)
-                bulk_g2s(ring.vec[s], arena + (int64_t)op.in * BF_NRHS,
-                         (uint32_t)nvec * BF_NRHS * 8u, &ring.full[s]);
+                bulk_g2s(ring.vec[s], arena + (int64_t)op.in * NR, (uint32_t)nvec * NR * 8u,
+                         &ring.full[s]);
         }
     }
 }
 
-// Tile product of one op into fragments e: e[mt][0..1] = result row
-// 8mt + lane/4, RHS 2(lane%4), 2(lane%4)+1 (lanes with lane%4 >= 2 carry the
-// n-padding and stay zero).
+// B fragment of n-group grp at k block ks: lane holds V[k = 4ks + q][rhs =
+// 8grp + g] (columns past the entry width are the n-padding)
+template <int NR>
+__device__ __forceinline__ double bfrag(const double *Vb, int ks, int grp, bool bl) {
+    return bl ? Vb[ks * 4 * NR + grp * 8] : 0.0;
+}
+
+// Tile product of one op into fragments e: e[grp][mt][0..1] = result row
+// 8mt + lane/4, RHS 8grp + 2(lane%4), +1.
+template <int NR>
 __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, const double *V,
-                                             const double *Z, int lane, double e[4][2]) {
+                                             const double *Z, int lane,
+                                             double e[Width<NR>::G][4][2]) {
+    constexpr int G = Width<NR>::G;
     const int g = lane >> 2, q = lane & 3, hi = lane >> 4;
     const int R4 = (op.R + 3) >> 2, C4 = (op.C + 3) >> 2;
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) e[mt][0] = e[mt][1] = 0.0;
-    // B fragment: lane holds V[k = 4ks + q][rhs = g] (rhs 4..7 are the n-padding)
-    const bool bl = g < 4;
-    const double *Vb = V + q * 4 + (g & 3);
+    for (int gr = 0; gr < G; ++gr)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) e[gr][mt][0] = e[gr][mt][1] = 0.0;
+    const bool bl = g < Width<NR>::GACT;
+    const double *Vb = V + q * NR + (NR >= 8 ? g : (g & (NR - 1)));
     if (op.R == BF_T && op.C == BF_T) {
         // full tile: straight-line, all fragment offsets are immediates
         if (op.kind == BF_OP_TILE_N) {
             const double *Ta = T + hi * (8 * 16) + (lane & 15);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
+                double av[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
-                    dmma(e[mt][0], e[mt][1], Ta[(mt * 16 + ks) * 16], b);
+                for (int mt = 0; mt < 4; ++mt) av[mt] = Ta[(mt * 16 + ks) * 16];
+#pragma unroll
+                for (int gr = 0; gr < G; ++gr) {
+                    const double b = bfrag<NR>(Vb, ks, gr, bl);
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);
+                }
             }
         } else {
             const double *Ta = T + hi * 16 + q * 4 + (g & 3);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
+                double av[4];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
-                    dmma(e[mt][0], e[mt][1], Ta[(ks * 8 + 2 * mt) * 16], b);
+                for (int mt = 0; mt < 4; ++mt) av[mt] = Ta[(ks * 8 + 2 * mt) * 16];
+#pragma unroll
+                for (int gr = 0; gr < G; ++gr) {
+                    const double b = bfrag<NR>(Vb, ks, gr, bl);
+#pragma unroll
+                    for (int mt = 0; mt < 4; ++mt) dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);
+                }
             }
         }
         return;
@@ -318,67 +355,52 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
             st[mt] = ok ? C4 * 16 : 0;
         }
     }
-    switch (MT) {
-        case 4:
-            for (int ks = 0; ks < K; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
-#pragma unroll
-                for (int mt = 0; mt < 4; ++mt) {
-                    dmma(e[mt][0], e[mt][1], *p[mt], b);
-                    p[mt] += st[mt];
-                }
-            }
-            break;
-        case 3:
-            for (int ks = 0; ks < K; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
-#pragma unroll
-                for (int mt = 0; mt < 3; ++mt) {
-                    dmma(e[mt][0], e[mt][1], *p[mt], b);
-                    p[mt] += st[mt];
-                }
-            }
-            break;
-        case 2:
-            for (int ks = 0; ks < K; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    dmma(e[mt][0], e[mt][1], *p[mt], b);
-                    p[mt] += st[mt];
-                }
-            }
-            break;
-        default:
-            for (int ks = 0; ks < K; ++ks) {
-                const double b = bl ? Vb[ks * 16] : 0.0;
-                dmma(e[0][0], e[0][1], *p[0], b);
-                p[0] += st[0];
-            }
-            break;
+#define BF_PARTIAL(NMT)                                                        \
+    for (int ks = 0; ks < K; ++ks) {                                           \
+        double av[NMT];                                                        \
+        _Pragma("unroll") for (int mt = 0; mt < NMT; ++mt) {                   \
+            av[mt] = *p[mt];                                                   \
+            p[mt] += st[mt];                                                   \
+        }                                                                      \
+        _Pragma("unroll") for (int gr = 0; gr < G; ++gr) {                     \
+            const double b = bfrag<NR>(Vb, ks, gr, bl);                        \
+            _Pragma("unroll") for (int mt = 0; mt < NMT; ++mt)                 \
+                dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);                   \
+        }                                                                      \
     }
+    switch (MT) {
+        case 4: BF_PARTIAL(4) break;
+        case 3: BF_PARTIAL(3) break;
+        case 2: BF_PARTIAL(2) break;
+        default: BF_PARTIAL(1) break;
+    }
+#undef BF_PARTIAL
 }
 
 // result m-tiles 0..3 of an op onto accumulator m-tiles SH..SH+3
-template <int SH>
-__device__ __forceinline__ void place_tiles(double acc[8][2], const double e[4][2]) {
+template <int G, int SH>
+__device__ __forceinline__ void place_tiles(double acc[G][8][2], const double e[G][4][2]) {
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
-        if (SH + mt < 8) {
-            acc[SH + mt][0] += e[mt][0];
-            acc[SH + mt][1] += e[mt][1];
-        }
+    for (int gr = 0; gr < G; ++gr)
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+            if (SH + mt < 8) {
+                acc[gr][SH + mt][0] += e[gr][mt][0];
+                acc[gr][SH + mt][1] += e[gr][mt][1];
+            }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) {
+template <int NR>
+__global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(StageArgs a) {
+    constexpr int G = Width<NR>::G, QACT = Width<NR>::QACT;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpRing &ring = reinterpret_cast<WarpRing *>(smem_raw)[warp];
+    WarpRing<NR> &ring = reinterpret_cast<WarpRing<NR> *>(smem_raw)[warp];
     {
         // zero the ring once: padded tile columns multiply stale vector
         // entries, which must therefore be finite
         double2 *z = reinterpret_cast<double2 *>(&ring);
-        const int n2 = (int)(offsetof(WarpRing, meta) / sizeof(double2));
+        const int n2 = (int)(offsetof(WarpRing<NR>, meta) / sizeof(double2));
         for (int i = lane; i < n2; i += 32) z[i] = make_double2(0.0, 0.0);
     }
     if (lane == 0) {
@@ -403,18 +425,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
     Rec q1 = advance(a, cur, lane);
     uint32_t seq_issue = 0, seq_use = 0;
     for (int s = 0; s < kStages && q0.valid; ++s) {
-        issue(a, ring, seq_issue % kStages, q0, g0, lane);
+        issue<NR>(a, ring, seq_issue % kStages, q0, g0, lane);
         ++seq_issue;
         q0 = q1;
         g0 = gather_src(a, q0, lane);
         q1 = advance(a, cur, lane);
     }
 
-    // task accumulator: acc[j] = slot 8j + lane/4, RHS 2(lane%4) .. +1,
-    // 64 slots (dense group tasks use the first 32)
-    double acc[8][2];
+    // task accumulator: acc[grp][j] = slot 8j + lane/4, RHS 8grp + 2(lane%4)
+    // .. +1, 64 slots (dense group tasks use the first 32)
+    double acc[G][8][2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int gr = 0; gr < G; ++gr)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[gr][j][0] = acc[gr][j][1] = 0.0;
 
     while (seq_use < seq_issue) {
         const int s = seq_use % kStages;
@@ -428,28 +452,32 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int jj = 8 * j + g - op.off;
-                if (q < 2 && jj >= 0 && jj < op.R) {
-                    const double2 v = *reinterpret_cast<const double2 *>(V + jj * 4 + 2 * q);
-                    acc[j][0] += v.x;
-                    acc[j][1] += v.y;
+                if (q < QACT && jj >= 0 && jj < op.R) {
+#pragma unroll
+                    for (int gr = 0; gr < G; ++gr) {
+                        const double2 v =
+                            *reinterpret_cast<const double2 *>(V + jj * NR + gr * 8 + 2 * q);
+                        acc[gr][j][0] += v.x;
+                        acc[gr][j][1] += v.y;
+                    }
                 }
             }
         } else {
-            double e[4][2];
-            tile_product(op, ring.tile[s], V, ring.zero, lane, e);
+            double e[G][4][2];
+            tile_product<NR>(op, ring.tile[s], V, ring.zero, lane, e);
             const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
             if (!lanemap && (op.off & 7) == 0) {
                 // result m-tile mt lands on slot m-tile mt + off/8
                 // (one case per shift keeps acc and e in registers)
                 switch (op.off >> 3) {
-                    case 0: place_tiles<0>(acc, e); break;
-                    case 1: place_tiles<1>(acc, e); break;
-                    case 2: place_tiles<2>(acc, e); break;
-                    case 3: place_tiles<3>(acc, e); break;
-                    case 4: place_tiles<4>(acc, e); break;
-                    case 5: place_tiles<5>(acc, e); break;
-                    case 6: place_tiles<6>(acc, e); break;
-                    default: place_tiles<7>(acc, e); break;
+                    case 0: place_tiles<G, 0>(acc, e); break;
+                    case 1: place_tiles<G, 1>(acc, e); break;
+                    case 2: place_tiles<G, 2>(acc, e); break;
+                    case 3: place_tiles<G, 3>(acc, e); break;
+                    case 4: place_tiles<G, 4>(acc, e); break;
+                    case 5: place_tiles<G, 5>(acc, e); break;
+                    case 6: place_tiles<G, 6>(acc, e); break;
+                    default: place_tiles<G, 7>(acc, e); break;
                 }
             } else {
                 // general placement through the warp's scratch rows
@@ -461,19 +489,26 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
                 const int MT = (width + 7) >> 3;
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
-                    if (mt < MT && q < 2)
-                        *reinterpret_cast<double2 *>(S + (8 * mt + g) * 4 + 2 * q) =
-                            make_double2(e[mt][0], e[mt][1]);
+                    if (mt < MT && q < QACT) {
+#pragma unroll
+                        for (int gr = 0; gr < G; ++gr)
+                            *reinterpret_cast<double2 *>(S + (8 * mt + g) * NR + gr * 8 + 2 * q) =
+                                make_double2(e[gr][mt][0], e[gr][mt][1]);
+                    }
                 __syncwarp();
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int sl = 8 * j + g;
                     const int src = lanemap ? (int)ring.map[s][sl]
                                             : sl - op.off;
-                    if (q < 2 && src >= 0 && src < width) {
-                        const double2 v = *reinterpret_cast<const double2 *>(S + src * 4 + 2 * q);
-                        acc[j][0] += v.x;
-                        acc[j][1] += v.y;
+                    if (q < QACT && src >= 0 && src < width) {
+#pragma unroll
+                        for (int gr = 0; gr < G; ++gr) {
+                            const double2 v =
+                                *reinterpret_cast<const double2 *>(S + src * NR + gr * 8 + 2 * q);
+                            acc[gr][j][0] += v.x;
+                            acc[gr][j][1] += v.y;
+                        }
                     }
                 }
                 __syncwarp();
@@ -485,16 +520,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const int sl = 8 * j + g;
-                if (q < 2 && sl < nout) {
-                    double *o = a.arena + ((int64_t)tm.x + (int64_t)sl * stride) * BF_NRHS + 2 * q;
-                    *reinterpret_cast<double2 *>(o) = make_double2(acc[j][0], acc[j][1]);
+                if (q < QACT && sl < nout) {
+                    double *o = a.arena + ((int64_t)tm.x + (int64_t)sl * stride) * NR + 2 * q;
+#pragma unroll
+                    for (int gr = 0; gr < G; ++gr)
+                        *reinterpret_cast<double2 *>(o + gr * 8) =
+                            make_double2(acc[gr][j][0], acc[gr][j][1]);
                 }
-                acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll
+                for (int gr = 0; gr < G; ++gr) acc[gr][j][0] = acc[gr][j][1] = 0.0;
             }
         }
         __syncwarp();
         if (q0.valid) {
-            issue(a, ring, seq_issue % kStages, q0, g0, lane);
+            issue<NR>(a, ring, seq_issue % kStages, q0, g0, lane);
             ++seq_issue;
             q0 = q1;
             g0 = gather_src(a, q0, lane);
@@ -505,16 +544,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_stage_kernel(StageArgs a) 
 
 }  // namespace
 
-static bool g_attr_set = false;
-
-int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st,
-                 int max_ctas) {
-    if (t1 <= t0) return 0;
-    const size_t smem = sizeof(WarpRing) * kWarps;
-    if (!g_attr_set) {
-        BF_CUDA(cudaFuncSetAttribute(alt_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        g_attr_set = true;
+template <int NR>
+static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, double *arena,
+                        cudaStream_t st, int max_ctas) {
+    constexpr int W = Width<NR>::WARPS;
+    static bool attr_set = false;
+    const size_t smem = sizeof(WarpRing<NR>) * W;
+    if (!attr_set) {
+        BF_CUDA(cudaFuncSetAttribute(alt_stage_kernel<NR>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
     }
     StageArgs a;
     a.tiles = pl->tiles;
@@ -522,17 +561,39 @@ int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStrea
     a.idx = pl->idx;
     a.maps = pl->maps;
     a.tasks = pl->tasks;
-    a.arena = pl->arena;
+    a.arena = arena;
     a.t0 = t0;
     a.ntasks = t1 - t0;
     a.counter = counter;
     BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
-    int64_t want = (a.ntasks + kWarps - 1) / kWarps;
+    int64_t want = (a.ntasks + W - 1) / W;
     const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;
     int grid = (int)(want < cap ? want : cap);
-    alt_stage_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+    alt_stage_kernel<NR><<<grid, W * 32, smem, st>>>(a);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
+    return 0;
+}
+
+int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st,
+                 int max_ctas) {
+    if (t1 <= t0) return 0;
+    return launch_stage<BF_NRHS>(pl, t0, t1, counter, pl->arena, st, max_ctas);
+}
+
+// All stages of one direction over a wide (16 RHS per entry) arena.
+int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) {
+    const std::vector<int64_t> &b = pl->stages[dir];
+    const int nst = (int)b.size() - 1;
+    if (pl->ncounters < nst) {
+        bfsht_set_error("plan counters not allocated");
+        return -3;
+    }
+    for (int s = 0; s < nst; ++s) {
+        if (b[s + 1] <= b[s]) continue;
+        int rc = launch_stage<BF_WIDE_NRHS>(pl, b[s], b[s + 1], pl->counters + s, arena, st, 0);
+        if (rc) return rc;
+    }
     return 0;
 }
 

@@ -21,6 +21,7 @@ struct bfsht_plan {
     // at layout[2o+p].y + r * layout[2o+p].x (fwd: row-major Yr; inv: halves)
     bf_half *layout_fwd = nullptr;
     bf_half *layout_inv = nullptr;
+    std::vector<bf_half> host_halves, host_layout_fwd;   // host copies
     double *arena = nullptr;
     std::vector<int64_t> stages[2];   // task bounds per stage (host)
     int32_t n = 0;                    // half size N
@@ -64,5 +65,10 @@ void bfsht_set_error(const std::string &msg);
 int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter,
                  cudaStream_t s, int max_ctas);
 int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
+int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);
+int bf_alt_fields(bfsht_plan *pl, int dir, int F, const double *in, double *out,
+                  const double *weights, double *work, cudaStream_t st);
+int bf_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
+                  double *work, cudaStream_t st);
 // sht.cu
 int bf_dft_prepare(bfsht_plan *pl, int64_t L);

@@ -31,7 +31,8 @@
 
 #define BF_T 32          /* max tile edge; dense group tasks write <= 32 entries */
 #define BF_SLOTS 64      /* max outputs per task (butterfly scatter tasks) */
-#define BF_NRHS 4        /* doubles per arena entry */
+#define BF_NRHS 4        /* doubles per arena entry (SHT path) */
+#define BF_WIDE_NRHS 16  /* doubles per entry of the batched-fields arena */
 
 enum bf_op_kind {
     BF_OP_TILE_N = 0,    /* lanes = tile rows, inputs = C entries  */

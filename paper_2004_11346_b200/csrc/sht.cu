@@ -626,6 +626,162 @@ int bf_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out, const 
     return 0;
 }
 
+// ------------------------------------------------------------------------
+// Batched fields (BASELINE config 4; SURVEY 8(b) "API extension"): F
+// complex fields per order sharing one plan, field-minor rows — forward
+// input (2N-m) x F and output 2N x F per order, plan after plan.  Pass p
+// carries fields 8p .. 8p+7 as the 16 real RHS of a wide arena entry, so
+// every DMMA uses its full n = 8 width and the payload is read once per 8
+// fields instead of once per field.
+namespace {
+
+constexpr int kW = BF_WIDE_NRHS;
+constexpr int kFPerPass = kW / 2;
+
+__global__ void fields_pack_kernel(int F, int f0, const bf_half *__restrict__ halves,
+                                   const int64_t *__restrict__ off, const double2 *__restrict__ in,
+                                   double *__restrict__ arena) {
+    const int o = blockIdx.y, f = threadIdx.x;
+    const int j = blockIdx.x * blockDim.y + threadIdx.y;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * o + par];
+        if (j >= h.ncols) continue;
+        double2 v = make_double2(0.0, 0.0);
+        if (f0 + f < F) v = in[(off[o] + (par == 0 ? 1 : 0) + 2 * (int64_t)j) * F + f0 + f];
+        *reinterpret_cast<double2 *>(arena + ((int64_t)h.x + j) * kW + 2 * f) = v;
+    }
+}
+
+__global__ void fields_assemble_kernel(int n, int F, int f0, const bf_half *__restrict__ layout,
+                                       const double *__restrict__ arena, double2 *__restrict__ out) {
+    const int o = blockIdx.y, f = threadIdx.x;
+    const int r = blockIdx.x * blockDim.y + threadIdx.y;
+    if (r >= n || f0 + f >= F) return;
+    const bf_half ho = layout[2 * o], he = layout[2 * o + 1];
+    double2 go = make_double2(0.0, 0.0), ge = go;
+    if (ho.ncols > 0)
+        go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)r * ho.x) * kW + 2 * f);
+    if (he.ncols > 0)
+        ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)r * he.x) * kW + 2 * f);
+    double2 *col = out + (int64_t)o * 2 * n * F + f0 + f;
+    col[(int64_t)(n + r) * F] = make_double2(ge.x + go.x, ge.y + go.y);
+    col[(int64_t)(n - 1 - r) * F] = make_double2(ge.x - go.x, ge.y - go.y);
+}
+
+__global__ void fields_fold_kernel(int n, int F, int f0, const bf_half *__restrict__ halves,
+                                   const double2 *__restrict__ in, const double *__restrict__ weights,
+                                   double *__restrict__ arena) {
+    const int o = blockIdx.y, f = threadIdx.x;
+    const int r = blockIdx.x * blockDim.y + threadIdx.y;
+    if (r >= n) return;
+    double2 up = make_double2(0.0, 0.0), lo = up;
+    if (f0 + f < F) {
+        const double2 *col = in + (int64_t)o * 2 * n * F + f0 + f;
+        up = col[(int64_t)(n + r) * F];
+        lo = col[(int64_t)(n - 1 - r) * F];
+    }
+    const double w = weights[n + r];
+    const bf_half ho = halves[2 * o], he = halves[2 * o + 1];
+    if (ho.ncols > 0)
+        *reinterpret_cast<double2 *>(arena + ((int64_t)ho.y + r) * kW + 2 * f) =
+            make_double2(w * (up.x - lo.x), w * (up.y - lo.y));
+    if (he.ncols > 0)
+        *reinterpret_cast<double2 *>(arena + ((int64_t)he.y + r) * kW + 2 * f) =
+            make_double2(w * (up.x + lo.x), w * (up.y + lo.y));
+}
+
+__global__ void fields_unpack_kernel(int F, int f0, const bf_half *__restrict__ halves,
+                                     const int64_t *__restrict__ off,
+                                     const double *__restrict__ arena, double2 *__restrict__ out) {
+    const int o = blockIdx.y, f = threadIdx.x;
+    const int j = blockIdx.x * blockDim.y + threadIdx.y;
+    if (f0 + f >= F) return;
+    for (int par = 0; par < 2; ++par) {
+        const bf_half h = halves[2 * o + par];
+        if (j >= h.ncols) continue;
+        out[(off[o] + (par == 0 ? 1 : 0) + 2 * (int64_t)j) * F + f0 + f] =
+            *reinterpret_cast<const double2 *>(arena + ((int64_t)h.x + j) * kW + 2 * f);
+    }
+}
+
+// Raw half apply (reference idbf_apply / _apply_half, butterfly.py:275-292,
+// alt.py:197-222): real row-major in (len_in x k) -> out (len_out x k),
+// columns c0 .. c0+15 of this pass.
+__global__ void half_load_kernel(int64_t base, int64_t stride, int len, int k, int c0,
+                                 const double *__restrict__ in, double *__restrict__ arena) {
+    const int r = blockIdx.x * blockDim.y + threadIdx.y, c = threadIdx.x;
+    if (r >= len) return;
+    arena[(base + r * stride) * kW + c] = (c0 + c < k) ? in[(int64_t)r * k + c0 + c] : 0.0;
+}
+
+__global__ void half_store_kernel(int64_t base, int64_t stride, int len, int k, int c0,
+                                  const double *__restrict__ arena, double *__restrict__ out) {
+    const int r = blockIdx.x * blockDim.y + threadIdx.y, c = threadIdx.x;
+    if (r >= len || c0 + c >= k) return;
+    out[(int64_t)r * k + c0 + c] = arena[(base + r * stride) * kW + c];
+}
+
+}  // namespace
+
+int bf_alt_fields(bfsht_plan *pl, int dir, int F, const double *in, double *out,
+                  const double *weights, double *work, cudaStream_t st) {
+    const int n = pl->n, no = pl->norders;
+    if (no == 0 || F == 0) return 0;
+    const dim3 blk(kFPerPass, 32);
+    const dim3 g((n + 31) / 32, no);
+    for (int f0 = 0; f0 < F; f0 += kFPerPass) {
+        if (dir == BFSHT_FORWARD) {
+            fields_pack_kernel<<<g, blk, 0, st>>>(F, f0, pl->halves, pl->order_off,
+                                                  reinterpret_cast<const double2 *>(in), work);
+            BF_CUDA(cudaGetLastError());
+            int rc = bf_alt_apply_wide(pl, dir, work, st);
+            if (rc) return rc;
+            fields_assemble_kernel<<<g, blk, 0, st>>>(n, F, f0, pl->layout_fwd, work,
+                                                      reinterpret_cast<double2 *>(out));
+            BF_CUDA(cudaGetLastError());
+        } else {
+            fields_fold_kernel<<<g, blk, 0, st>>>(n, F, f0, pl->halves,
+                                                  reinterpret_cast<const double2 *>(in), weights,
+                                                  work);
+            BF_CUDA(cudaGetLastError());
+            int rc = bf_alt_apply_wide(pl, dir, work, st);
+            if (rc) return rc;
+            fields_unpack_kernel<<<g, blk, 0, st>>>(F, f0, pl->halves, pl->order_off, work,
+                                                    reinterpret_cast<double2 *>(out));
+            BF_CUDA(cudaGetLastError());
+        }
+        pl->launches += 2;
+    }
+    return 0;
+}
+
+int bf_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
+                  double *work, cudaStream_t st) {
+    const bf_half hf = pl->host_halves[half];
+    const bf_half lay = pl->host_layout_fwd[half];
+    // forward: columns in (x region), rows out (Yr: base lay.y, stride lay.x)
+    // inverse: rows in (y region), columns out (x region)
+    const int64_t in_base = dir == BFSHT_FORWARD ? hf.x : hf.y;
+    const int64_t in_stride = 1;
+    const int in_len = dir == BFSHT_FORWARD ? hf.ncols : pl->n;
+    const int64_t out_base = dir == BFSHT_FORWARD ? lay.y : hf.x;
+    const int64_t out_stride = dir == BFSHT_FORWARD ? lay.x : 1;
+    const int out_len = dir == BFSHT_FORWARD ? pl->n : hf.ncols;
+    const dim3 blk(kW, 16);
+    for (int c0 = 0; c0 < k; c0 += kW) {
+        half_load_kernel<<<(in_len + 15) / 16, blk, 0, st>>>(in_base, in_stride, in_len, k, c0, in,
+                                                              work);
+        BF_CUDA(cudaGetLastError());
+        int rc = bf_alt_apply_wide(pl, dir, work, st);
+        if (rc) return rc;
+        half_store_kernel<<<(out_len + 15) / 16, blk, 0, st>>>(out_base, out_stride, out_len, k,
+                                                                c0, work, out);
+        BF_CUDA(cudaGetLastError());
+        pl->launches += 2;
+    }
+    return 0;
+}
+
 int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *in, double *out,
                 cudaStream_t st) {
     int rc = bf_dft_prepare(pl, L);
