@@ -62,6 +62,9 @@ def parse():
                     help="c2: SHT fwd+inv (default, the headline); c4: batched "
                          "forward ALT of 64 fields (wide DMMA engine)")
     ap.add_argument("--fields", type=int, default=64)
+    ap.add_argument("--regen", type=float, default=0.0,
+                    help="fraction of full-height dense turning tiles regenerated "
+                         "on the GPU from recurrence seeds (SURVEY f1)")
     return ap.parse_args()
 
 
@@ -298,10 +301,10 @@ def run_ours(args):
     if world == 1:
         eng = ShtDevice.__new__(ShtDevice)
         eng.n = n
-        eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights)
+        eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights, regen=args.regen)
         runner = D.SingleRunner(eng)
     else:
-        runner = D.ShardedSht(n, plans, orders, rank, world)
+        runner = D.ShardedSht(n, plans, orders, rank, world, regen=args.regen)
     torch.cuda.synchronize()
     t_up = time.time() - t0
 
@@ -364,6 +367,17 @@ def run_ours(args):
                 "alt_fwd_ms": alt["fwd_ms"], "alt_inv_ms": alt["inv_ms"],
                 "alg_bytes_per_direction": alt_bytes_all / world,
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}
+    if args.regen > 0:
+        # B_ALT with and without the regenerated tiles
+        hb = float(runner.hbm_bytes())
+        pk = runner.dp.packed
+        roofline["regen"] = {
+            "fraction": args.regen, "tiles": pk.regen_tiles,
+            "values_regenerated": pk.stats["regen_values"],
+            "hbm_bytes_per_direction_rank0": hb,
+            "hbm_GBps_rank0": hb / (alt_ms * 1e-3) / 1e9,
+            "note": "achieved/frac count every reference value (algorithmic); "
+                    "regenerated values do not cross HBM"}
 
     # ------------------------------------------------ e2e via the host API
     e2e = runner.time_e2e(flat, args.steps, args.warmup, barrier)
@@ -463,7 +477,7 @@ def run_fields(args):
     n, nf = args.n, args.fields
     plans = plan_orders(n, range(2 * n), SamplingConfig(tolerance=args.tol),
                         processes=args.plan_procs or (os.cpu_count() or 1))
-    dp = DevicePlan(plans, weights=plans[0].quadrature.weights)
+    dp = DevicePlan(plans, weights=plans[0].quadrature.weights, regen=args.regen)
     rows = dp.coeff_len
     rng = np.random.default_rng(4)
     host = torch.empty((rows, nf), dtype=torch.complex128).pin_memory()

@@ -66,6 +66,17 @@ typedef struct {
     const int32_t *ncols;       /* 2*norders: (odd, even) columns, 0=absent */
     int64_t nblocks;
     const bfsht_block *blocks;
+    /* On-GPU regeneration of dense turning tiles.  A
+     * fraction regen in [0, 1] of the full-height (32-row) tiles of kind-2
+     * blocks is stored as recurrence seeds (per row: p_prev, p_cur, 2^e at
+     * the tile's first degree) instead of values; the engine re-runs the
+     * reference recurrence (kernels/_recur_cy.pyx:18-67) bit for bit.
+     * Needs the nodes and start values below; regen = 0 ignores them. */
+    double regen;
+    const double *x_pos;        /* n positive nodes, ascending (AltMatrixSpec.x_pos) */
+    const double *mant0;        /* norders x n: start mantissas (common.py:65-77) */
+    const int32_t *exp0;        /* norders x n: start exponents                */
+    double mag_min;             /* flush threshold of emitted values (MAG_MIN)  */
 } bfsht_manifest;
 
 typedef struct bfsht_packed bfsht_packed;   /* opaque host-side packed plan */
@@ -80,10 +91,23 @@ int bfsht_pack_plan(const bfsht_manifest *man, int threads,
  * 9 payload values (sum of stored reference values), 10 arena entry of the
  * row-major forward node array Yr[r][order][parity], 11 butterfly blocks, 12 low-rank blocks, 13 dense blocks,
  * 14 half-size N, 15 number of order plans, 16/17 index of the free
- * (dependency-free dense) stage of the forward/inverse direction */
+ * (dependency-free dense) stage of the forward/inverse direction,
+ * 18 regenerated tiles, 19 reference values they replace (not stored),
+ * 20 doubles of the recurrence-coefficient table, 21 doubles of x_pos,
+ * 22 bit pattern of mag_min (double) */
 #define BFSHT_INFO_LEN 24
 int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_LEN]);
-int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]);
+/* arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves, 6/7 stage
+ * bounds fwd/inv, 8 recurrence coefficients (alpha, beta pairs), 9 x_pos */
+int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[10]);
+/* alpha_s, beta_s (s = 0 .. k_max-m-1) of the degree recurrence
+ * (kernels/common.py:37-53), interleaved; for tests of the seed path. */
+int bfsht_rec_coeffs(int64_t m, int64_t k_max, double *out);
+/* Regenerate one seeded tile on the host exactly as the engine does (test
+ * oracle of the device generation): seed block at `seed`, R x C tile in
+ * the 4x4-block layout into out (bf_tile_doubles(R, C) doubles). */
+int bfsht_regen_tile_host(const double *seed, int R, int C, const double *rec,
+                          const double *x_pos, double mag_min, double *out);
 void bfsht_packed_free(bfsht_packed *p);
 
 const char *bfsht_last_error(void);
@@ -96,10 +120,12 @@ typedef struct bfsht_plan bfsht_plan;       /* opaque device plan */
 int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out);
 /* Device arrays already resident (e.g. allocated through torch), borrowed:
  * dev[0..5] = tiles, ops, idx, maps, tasks, halves (bfsht_packed_arrays
- * order), dev[6] = vector arena (info[5] x 4 doubles); host[5..7] = host
- * copies of halves and the two stage-bound arrays. */
+ * order), dev[6] = vector arena (info[5] x 4 doubles), dev[7] = recurrence
+ * coefficients, dev[8] = x_pos (both only read by regenerated tiles, may
+ * be NULL when info[18] == 0); host[5..7] = host copies of halves and the
+ * two stage-bound arrays. */
 int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
-                    void *const dev[8], bfsht_plan **out);
+                    void *const dev[10], bfsht_plan **out);
 void bfsht_plan_free(bfsht_plan *pl);
 /* Scheduling knobs: overlap = run the dependency-free dense stage on its
  * own SMs concurrently with the butterfly/low-rank chain (default 1);

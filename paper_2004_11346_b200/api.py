@@ -70,11 +70,11 @@ class DevicePlan:
     the vector arena) are torch tensors; the native handle borrows them.
     """
 
-    def __init__(self, plans, device=None, packed=None, weights=None):
+    def __init__(self, plans, device=None, packed=None, weights=None, regen=0.0):
         torch = _torch()
         self.lib = native.cuda()
         plans = list(plans)
-        self.packed = pack_plans(plans) if packed is None else packed
+        self.packed = pack_plans(plans, regen=regen) if packed is None else packed
         pk = self.packed
         self.n = pk.n
         self.orders = [int(m) for m in pk.orders]
@@ -94,6 +94,8 @@ class DevicePlan:
                 up(pk.maps if pk.maps.size else np.zeros(32, np.int8)),
                 up(pk.tasks.view(np.int32) if pk.tasks.size else np.zeros(4, np.int32)),
                 up(pk.halves.view(np.int32)),
+                up(pk.rec if pk.rec.size else np.zeros(2)),
+                up(pk.xpos if pk.xpos.size else np.zeros(2)),
             ]
             self.arena = torch.zeros((max(pk.stats["arena"], 1), NRHS),
                                      dtype=torch.float64, device=self.device)
@@ -110,10 +112,12 @@ class DevicePlan:
             host[5] = self._host_halves.ctypes.data
             host[6] = self._sf.ctypes.data
             host[7] = self._si.ctypes.data
-            dev = (ctypes.c_void_p * 8)()
-            for i, t in enumerate(self._dev):
+            dev = (ctypes.c_void_p * 10)()
+            for i, t in enumerate(self._dev[:6]):
                 dev[i] = t.data_ptr()
             dev[6] = self.arena.data_ptr()
+            dev[7] = self._dev[6].data_ptr()
+            dev[8] = self._dev[7].data_ptr()
             h = ctypes.c_void_p()
             check(self.lib, self.lib.bfsht_plan_wrap(info, host, dev,
                                                      ctypes.byref(h)),

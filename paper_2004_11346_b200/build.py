@@ -1,7 +1,8 @@
 """In-tree build of the native libraries (``python -m paper_2004_11346_b200.build``).
 
 * libbfsht_host.so: gcc/g++ -O3 -ffp-contract=off (the recurrence must not
-  contract into FMAs, see csrc/recur.c), plus the C++ plan packer.
+  contract into FMAs, see csrc/recur.h), plus the C++ plan packer (which
+  runs the same recurrence for regeneration seeds).
 * libbfsht_b200.so: nvcc for sm_100a only, -lineinfo so ncu source pages map
   back to csrc/*.cu.  The C ABI is declared in include/bfsht_b200.h.
 """
@@ -35,7 +36,8 @@ def build_host(force=False):
     c_src = [os.path.join(CSRC, "recur.c")]
     cpp_src = [os.path.join(CSRC, f) for f in ("packer.cpp",)
                if os.path.exists(os.path.join(CSRC, f))]
-    deps = c_src + cpp_src + [os.path.join(INCLUDE, "bfsht_b200.h")]
+    deps = c_src + cpp_src + [os.path.join(INCLUDE, "bfsht_b200.h")] + [
+        os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
     if not force and not _stale(out, [d for d in deps if os.path.exists(d)]):
         return out
     objs = []
@@ -46,8 +48,8 @@ def build_host(force=False):
         objs.append(obj)
     for src in cpp_src:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
-        _run(["g++", "-O3", "-fPIC", "-std=c++17", "-fopenmp", "-I", INCLUDE,
-              "-c", src, "-o", obj])
+        _run(["g++", "-O3", "-ffp-contract=off", "-fPIC", "-std=c++17", "-fopenmp",
+              "-I", INCLUDE, "-c", src, "-o", obj])
         objs.append(obj)
     _run(["g++", "-shared", "-fopenmp", "-o", out] + objs + ["-lm"])
     return out
@@ -75,8 +77,8 @@ def build_cuda(force=False):
     # the packer rides along so C users get pack + upload + apply in one .so
     pk = os.path.join(CSRC, "packer.cpp")
     pobj = os.path.join(CSRC, "packer.cuda.o")
-    _run(["g++", "-O3", "-fPIC", "-std=c++17", "-fopenmp", "-I", INCLUDE,
-          "-c", pk, "-o", pobj])
+    _run(["g++", "-O3", "-ffp-contract=off", "-fPIC", "-std=c++17", "-fopenmp",
+          "-I", INCLUDE, "-c", pk, "-o", pobj])
     objs.append(pobj)
     _run([NVCC] + ARCH + ["-shared", "-o", out] + objs + ["-lgomp"])
     return out

@@ -90,17 +90,20 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
         g_err = "bad packed plan";
         return -1;
     }
-    const void *arr[8];
+    const void *arr[10];
     bfsht_packed_arrays(p, arr);
-    const size_t sz[6] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
+    // device copies of arrays 0..5 and 8..9 (stage bounds stay on the host)
+    const int which[8] = {0, 1, 2, 3, 4, 5, 8, 9};
+    const size_t sz[8] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
                           (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
                           (size_t)pl->info[4] * sizeof(bf_task),
-                          (size_t)pl->info[6] * sizeof(bf_half)};
-    void *dev[6];
-    for (int i = 0; i < 6; ++i) {
+                          (size_t)pl->info[6] * sizeof(bf_half),
+                          (size_t)pl->info[20] * 8, (size_t)pl->info[21] * 8};
+    void *dev[8];
+    for (int i = 0; i < 8; ++i) {
         dev[i] = nullptr;
         if (cudaMalloc(&dev[i], sz[i] ? sz[i] : 16) != cudaSuccess ||
-            (sz[i] && cudaMemcpy(dev[i], arr[i], sz[i], cudaMemcpyHostToDevice) != cudaSuccess)) {
+            (sz[i] && cudaMemcpy(dev[i], arr[which[i]], sz[i], cudaMemcpyHostToDevice) != cudaSuccess)) {
             g_err = "device allocation/copy failed";
             for (int j = 0; j <= i; ++j) cudaFree(dev[j]);
             delete pl;
@@ -121,6 +124,8 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     pl->maps = (const int8_t *)dev[3];
     pl->tasks = (const bf_task *)dev[4];
     pl->halves = (const bf_half *)dev[5];
+    pl->rec = (const double *)dev[6];
+    pl->xpos = (const double *)dev[7];
     pl->arena = (double *)arena;
     int rc = finish_plan(pl, (const bf_half *)arr[5], (const int64_t *)arr[6],
                          (const int64_t *)arr[7]);
@@ -132,8 +137,8 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     return 0;
 }
 
-int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8], void *const dev[8],
-                    bfsht_plan **out) {
+int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
+                    void *const dev[10], bfsht_plan **out) {
     if (!info || !host || !dev || !out) {
         g_err = "null argument";
         return -1;
@@ -147,6 +152,13 @@ int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8
     pl->tasks = (const bf_task *)dev[4];
     pl->halves = (const bf_half *)dev[5];
     pl->arena = (double *)dev[6];
+    pl->rec = (const double *)dev[7];
+    pl->xpos = (const double *)dev[8];
+    if (info[18] > 0 && (!pl->rec || !pl->xpos)) {
+        delete pl;
+        g_err = "plan has regenerated tiles but no coefficient table / nodes";
+        return -1;
+    }
     int rc = finish_plan(pl, (const bf_half *)host[5], (const int64_t *)host[6],
                          (const int64_t *)host[7]);
     if (rc) {

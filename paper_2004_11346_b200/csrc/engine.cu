@@ -31,7 +31,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <cstring>
+
 #include "engine.cuh"
+#include "recur.h"
 
 namespace {
 
@@ -137,6 +140,9 @@ struct StageArgs {
     double *arena;
     int64_t t0, ntasks;
     int *counter;
+    const double *rec;     // recurrence coefficients (regenerated tiles)
+    const double *xpos;    // positive nodes
+    double mag_min;
 };
 
 __device__ __forceinline__ bf_op load_op(const bf_op *p) {
@@ -217,7 +223,91 @@ __device__ __forceinline__ int gather_src(const StageArgs &a, const Rec &r, int 
 }
 
 __device__ __forceinline__ uint32_t tile_bytes(const bf_op &op) {
-    return (uint32_t)bf_tile_doubles(op.R, op.C) * 8u;
+    return (op.flags & BF_OPF_REGEN) ? (uint32_t)bf_seed_doubles(op.R) * 8u
+                                     : (uint32_t)bf_tile_doubles(op.R, op.C) * 8u;
+}
+
+// Where a tile's bytes land in its ring slot: values at the start; a seed
+// block at the end, so the regenerated values can be written from the
+// start once every lane holds its row's seed.
+__device__ __forceinline__ uint32_t tile_dst(const bf_op &op) {
+    return (op.flags & BF_OPF_REGEN) ? (uint32_t)(kTileDoubles - bf_seed_doubles(op.R)) : 0u;
+}
+
+// value p * 2^e flushed to 0 below mag_min, exactly ldexp(p, e) then the
+// flush (recur.c emit): a normal p with a normal result only shifts its
+// exponent field; results below 2^-1022 are under mag_min (~2^-1010) anyway
+__device__ __forceinline__ double emit_value(double p, int e, double mag_min) {
+    const long long b = __double_as_longlong(p);
+    const int ef = (int)((b >> 52) & 0x7ff);
+    const int ne = ef + e;
+    double v;
+    if (ef != 0 && ne >= 1 && ne <= 2046)
+        v = __longlong_as_double(b + ((long long)e << 52));
+    else if (ef != 0 && ne < 1)
+        v = 0.0;
+    else
+        v = ldexp(p, e);   // zero / subnormal p, or overflow: rare
+    return fabs(v) < mag_min ? 0.0 : v;
+}
+
+// Regenerate a dense turning tile in place from its seed block:
+// lane r re-runs row r's degree recurrence exactly as the planner did
+// (recur.h; pkg/src/bfsht/kernels/_recur_cy.pyx:45-66), two steps per
+// column (degrees of one parity), emitting ldexp(p, e) flushed below
+// MAG_MIN — the stored values bit for bit (tests/test_regen_pack.py,
+// tests/test_gpu_regen.py).  The tile's step coefficients arrive in one
+// coalesced load (lane c holds column c's two steps) and are broadcast by
+// shuffles; four columns are emitted per 32-byte shared store.  Padding
+// rows / columns are written as zeros.
+__device__ __noinline__ void regen_tile(const double *__restrict__ rec,
+                                        const double *__restrict__ xpos, double mag_min, int R,
+                                        int C, double *T, int lane) {
+    const int C4 = (C + 3) >> 2, R4 = (R + 3) >> 2;
+    const double *sb = T + kTileDoubles - bf_seed_doubles(R);
+    const int r_a = __double2loint(sb[0]);
+    const long long rb = __double_as_longlong(sb[1]);
+    double pp = 0.0, pc = 0.0, x = 0.0;
+    int e = 0;
+    if (lane < R) {
+        pp = sb[2 + 3 * lane];
+        pc = sb[3 + 3 * lane];
+        e = (int)sb[4 + 3 * lane];
+        x = __ldg(xpos + r_a + lane);
+    }
+    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+    if (lane + 1 < C) {
+        const double2 *ab = reinterpret_cast<const double2 *>(rec + rb) + 2 * lane;
+        s0 = __ldg(ab);
+        s1 = __ldg(ab + 1);
+    }
+    __syncwarp();
+    const bool live = lane < R;
+    double *row = T + (lane >> 2) * C4 * 16 + (lane & 3) * 4;
+    for (int cb = 0; cb < C4; ++cb) {
+        double v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int c = 4 * cb + i;
+            v[i] = (live && c < C) ? emit_value(pc, e, mag_min) : 0.0;
+            if (c + 1 < C) {
+                const double a0 = __shfl_sync(0xffffffffu, s0.x, c);
+                const double b0 = __shfl_sync(0xffffffffu, s0.y, c);
+                const double a1 = __shfl_sync(0xffffffffu, s1.x, c);
+                const double b1 = __shfl_sync(0xffffffffu, s1.y, c);
+                if (live) {
+                    bfr_step(x, a0, b0, &pp, &pc, &e);
+                    bfr_step(x, a1, b1, &pp, &pc, &e);
+                }
+            }
+        }
+        if (lane < R4 * 4) {
+            double2 *d = reinterpret_cast<double2 *>(row + cb * 16);
+            d[0] = make_double2(v[0], v[1]);
+            d[1] = make_double2(v[2], v[3]);
+        }
+    }
+    __syncwarp();
 }
 
 // Issue the loads of one op into ring slot s (whole warp).
@@ -262,7 +352,7 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing<NR> &ring, in
         fence_proxy_async();
         mbar_arrive_tx(&ring.full[s], bytes);
         if (op.kind != BF_OP_ADD) {
-            bulk_g2s(ring.tile[s], a.tiles + op.tile, tile_bytes(op), &ring.full[s]);
+            bulk_g2s(ring.tile[s] + tile_dst(op), a.tiles + op.tile, tile_bytes(op), &ring.full[s]);
             if (!gather)
                 bulk_g2s(ring.vec[s], arena + (int64_t)op.in * NR, (uint32_t)nvec * NR * 8u,
                          &ring.full[s]);
@@ -463,6 +553,8 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
                 }
             }
         } else {
+            if (op.flags & BF_OPF_REGEN)
+                regen_tile(a.rec, a.xpos, a.mag_min, op.R, op.C, ring.tile[s], lane);
             double e[G][4][2];
             tile_product<NR>(op, ring.tile[s], V, ring.zero, lane, e);
             const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
@@ -565,6 +657,9 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
     a.t0 = t0;
     a.ntasks = t1 - t0;
     a.counter = counter;
+    a.rec = pl->rec;
+    a.xpos = pl->xpos;
+    std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
     BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     int64_t want = (a.ntasks + W - 1) / W;
     const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;

@@ -17,6 +17,8 @@ struct bfsht_plan {
     const int8_t *maps = nullptr;
     const bf_task *tasks = nullptr;
     const bf_half *halves = nullptr;
+    const double *rec = nullptr;      // recurrence coefficients (regenerated tiles)
+    const double *xpos = nullptr;     // positive nodes (regenerated tiles)
     // node-half addressing for the DFT stage: entry (order o, parity p, row r)
     // at layout[2o+p].y + r * layout[2o+p].x (fwd: row-major Yr; inv: halves)
     bf_half *layout_fwd = nullptr;

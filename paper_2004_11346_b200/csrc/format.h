@@ -42,8 +42,25 @@ enum bf_op_kind {
 
 enum bf_op_flags {
     BF_OPF_GATHER = 1,   /* inputs through idx[in + i], else in + i (idx < 0: none) */
-    BF_OPF_LANEMAP = 2   /* outputs through maps[aux*32 + slot] (tile lane or -1) */
+    BF_OPF_LANEMAP = 2,  /* outputs through maps[aux*32 + slot] (tile lane or -1) */
+    BF_OPF_REGEN = 4     /* `tile` is a seed block: regenerate the values (f1) */
 };
+
+/* Seed block of a regenerated dense tile (R rows, full 32-wide at most):
+ *   double[0]: int32 first row r_a (index into x_pos), int32 unused
+ *   double[1]: int64 offset (doubles) in the coefficient table of the step
+ *              leaving the tile's first degree: alpha at [+0], beta at [+1],
+ *              next step at [+2], [+3], ...
+ *   double[2 + 3r .. 4 + 3r]: row r's p_prev, p_cur and exponent e (exact,
+ *              as a double) at that degree
+ * padded to a multiple of 16 doubles (128 B). */
+static inline
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+int64_t bf_seed_doubles(int R) {
+    return ((int64_t)(2 + 3 * R) + 15) / 16 * 16;
+}
 
 typedef struct {
     int64_t tile;        /* element offset of the tile in the tile store  */

@@ -28,6 +28,7 @@
 //    all segments sharing a range summed in one task.  The same tiles serve
 //    both, so a factor is stored once.  Depth-0 chains are dense blocks.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -41,6 +42,7 @@
 
 #include "bfsht_b200.h"
 #include "format.h"
+#include "recur.h"
 
 static thread_local std::string g_err;
 
@@ -61,6 +63,11 @@ struct bfsht_packed {
     int64_t n = 0, norders = 0;
     int32_t yr = 0;   // row-major forward node array Yr[r][order][parity]
     int32_t free_stage[2] = {-1, -1};   // dependency-free dense stage per direction
+    // regenerated dense tiles (f1)
+    int64_t n_regen = 0, regen_values = 0;
+    std::vector<double> rec;            // per order: (alpha, beta) for s = 0 .. 2N-m-1
+    std::vector<double> xpos;
+    double mag_min = 0.0;
 };
 
 namespace {
@@ -70,6 +77,13 @@ struct TileJob {
     int R, C;
     const double *src;
     int64_t rs, cs;  // element (r, c) = src[r*rs + c*cs]
+};
+
+struct SeedJob {
+    int64_t dst;      // seed block offset in the tile store
+    int h;            // half index (2 * order + parity)
+    int r_a, R;       // rows
+    int64_t c_a;      // first half column
 };
 
 struct TaskBuild {
@@ -253,6 +267,9 @@ struct Packer {
     bfsht_packed &P;
     const bfsht_manifest &M;
     std::vector<TileJob> jobs;
+    std::vector<SeedJob> seeds;
+    std::vector<int64_t> rec_base;      // per order: offset of its table in P.rec
+    int64_t regen_candidates = 0;
     std::vector<std::unique_ptr<std::vector<double>>> keep;  // temp sources
     // tasks by direction and stage
     std::vector<std::vector<TaskBuild>> stages[2];
@@ -320,19 +337,106 @@ struct Packer {
     }
 
     // ---------------------------------------------------------- dense
+    // Regeneration choice for one tile of a turning block: full-height
+    // tiles only (one recurrence chain per lane covers 32 rows), spread
+    // evenly over the candidates in packing order.
+    bool want_regen(int R) {
+        if (M.regen <= 0.0 || R != BF_T) return false;
+        const double f = M.regen >= 1.0 ? 1.0 : M.regen;
+        const int64_t k = regen_candidates++;
+        return (int64_t)((double)(k + 1) * f) > (int64_t)((double)k * f);
+    }
+
     void dense(int h_idx, const double *a, int64_t lda, int64_t r0, int64_t r1,
-               int64_t c0, int64_t c1) {
+               int64_t c0, int64_t c1, bool turning = false) {
         const bf_half &hf = P.halves[h_idx];
         for (auto rr : cuts(r0, r1))
             for (auto cc : cuts(c0, c1)) {
                 int R = (int)(rr.second - rr.first), C = (int)(cc.second - cc.first);
-                int64_t t = alloc_tile(R, C, a + (rr.first - r0) * lda + (cc.first - c0), lda, 1);
+                int flags = 0;
+                int64_t t;
+                if (turning && want_regen(R)) {
+                    t = P.n_tiles;
+                    P.n_tiles += bf_seed_doubles(R);
+                    seeds.push_back({t, h_idx, (int)rr.first, R, cc.first});
+                    flags = BF_OPF_REGEN;
+                    P.n_regen++;
+                    P.regen_values += (int64_t)R * C;
+                } else {
+                    t = alloc_tile(R, C, a + (rr.first - r0) * lda + (cc.first - c0), lda, 1);
+                }
                 int g = (int)(rr.first / BF_T), gc = (int)(cc.first / BF_T);
                 fwd_groups[h_idx][g].push_back(mk(BF_OP_TILE_N, t, hf.x + (int32_t)cc.first, R, C,
-                                                  (int)(rr.first - (int64_t)g * BF_T)));
+                                                  (int)(rr.first - (int64_t)g * BF_T), flags));
                 inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, C,
-                                                   (int)(cc.first - (int64_t)gc * BF_T)));
+                                                   (int)(cc.first - (int64_t)gc * BF_T), flags));
             }
+    }
+
+    // Recurrence-coefficient tables and per-row seeds of the regenerated
+    // tiles: the states (p_prev, p_cur, e) at each tile's first degree,
+    // from the reference start values by the same no-FMA step the table
+    // was built with, so the regenerated values are the stored ones.
+    void build_rec() {
+        const int64_t n2 = 2 * (int64_t)M.n;
+        rec_base.assign(M.norders + 1, 0);
+        for (int o = 0; o < M.norders; ++o) rec_base[o + 1] = rec_base[o] + 2 * (n2 - M.m[o]);
+        P.rec.assign((size_t)rec_base[M.norders], 0.0);
+        for (int o = 0; o < M.norders; ++o)
+            for (int64_t s = 0; s < n2 - M.m[o]; ++s)
+                bfr_coeffs(M.m[o], M.m[o] + s, &P.rec[rec_base[o] + 2 * s],
+                           &P.rec[rec_base[o] + 2 * s + 1]);
+        P.xpos.assign(M.x_pos, M.x_pos + M.n);
+        P.mag_min = M.mag_min;
+    }
+
+    void fill_seeds(int threads) {
+        if (seeds.empty()) return;
+        if (!M.x_pos || !M.mant0 || !M.exp0) throw std::runtime_error("regen needs x_pos and start values");
+        // per half and 32-row band: every seed job, by first degree
+        std::map<std::pair<int, int>, std::vector<size_t>> bands;
+        for (size_t i = 0; i < seeds.size(); ++i) bands[{seeds[i].h, seeds[i].r_a}].push_back(i);
+        std::vector<std::pair<std::pair<int, int>, std::vector<size_t>>> work(bands.begin(), bands.end());
+        double *T = P.tiles.get();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads)
+        for (int64_t wi = 0; wi < (int64_t)work.size(); ++wi) {
+            const int h = work[wi].first.first, r_a = work[wi].first.second;
+            std::vector<size_t> js = work[wi].second;
+            const int o = h / 2, par = h % 2;
+            const int64_t m = M.m[o], offset = par == 0 ? 1 : 0;
+            std::sort(js.begin(), js.end(), [&](size_t x, size_t y) { return seeds[x].c_a < seeds[y].c_a; });
+            const double *rec = P.rec.data() + rec_base[o];
+            int R = 0;
+            for (size_t j : js) {
+                const SeedJob &sj = seeds[j];
+                R = std::max(R, sj.R);
+                double *sb = T + sj.dst;
+                std::memset(sb, 0, sizeof(double) * bf_seed_doubles(sj.R));
+                const int64_t k_a = m + offset + 2 * sj.c_a;
+                int32_t hdr[2] = {sj.r_a, 0};
+                std::memcpy(sb, hdr, sizeof(hdr));
+                const int64_t rb = rec_base[o] + 2 * (k_a - m);
+                std::memcpy(sb + 1, &rb, sizeof(rb));
+            }
+            for (int r = 0; r < R; ++r) {
+                const int row = r_a + r;
+                const double xr = M.x_pos[row];
+                double pp = 0.0, pc = M.mant0[(int64_t)o * M.n + row];
+                int e = M.exp0[(int64_t)o * M.n + row];
+                int64_t k = m;
+                for (size_t j : js) {
+                    const SeedJob &sj = seeds[j];
+                    const int64_t k_a = m + offset + 2 * sj.c_a;
+                    for (; k < k_a; ++k) bfr_step(xr, rec[2 * (k - m)], rec[2 * (k - m) + 1], &pp, &pc, &e);
+                    if (r < sj.R) {
+                        double *sr = T + sj.dst + 2 + 3 * r;
+                        sr[0] = pp;
+                        sr[1] = pc;
+                        sr[2] = (double)e;
+                    }
+                }
+            }
+        }
     }
 
     // -------------------------------------------------------- low-rank
@@ -552,6 +656,11 @@ struct Packer {
                     hf.x = hf.y = -1;
                 }
             }
+        if (M.regen > 0.0) {
+            if (!M.x_pos || !M.mant0 || !M.exp0 || !(M.mag_min > 0.0))
+                throw std::runtime_error("regen needs x_pos, start values and mag_min");
+            build_rec();
+        }
         // butterfly segmentation in parallel (the heavy part)
         std::vector<std::vector<FactorSegs>> segs((size_t)M.nblocks);
         std::vector<std::string> errs((size_t)M.nblocks);
@@ -591,7 +700,7 @@ struct Packer {
             if (b.kind == 2) {
                 P.n_dn++;
                 P.payload_values += h * w;
-                dense(h_idx, b.a, w, b.r0, b.r1, b.c0, b.c1);
+                dense(h_idx, b.a, w, b.r0, b.r1, b.c0, b.c1, true);
             } else if (b.kind == 1) {
                 P.n_lr++;
                 P.payload_values += (h + w + 1) * (int64_t)b.rank;
@@ -778,6 +887,7 @@ struct Packer {
                     dst[bf_tile_index(r, c, C4)] = t.src[r * t.rs + c * t.cs];
             (void)R4;
         }
+        fill_seeds(threads);
     }
 };
 
@@ -822,12 +932,18 @@ extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_
     info[13] = p->n_dn;
     info[14] = p->n;
     info[15] = p->norders;
+    info[18] = p->n_regen;
+    info[19] = p->regen_values;
+    info[20] = (int64_t)p->rec.size();
+    info[21] = (int64_t)p->xpos.size();
+    std::memcpy(&info[22], &p->mag_min, sizeof(double));
     return 0;
 }
 
 // arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves,
-//         6 stage bounds fwd (int64, stages+1), 7 stage bounds inv
-extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8]) {
+//         6 stage bounds fwd (int64, stages+1), 7 stage bounds inv,
+//         8 recurrence coefficients, 9 x_pos
+extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[10]) {
     if (!p) return -1;
     arrays[0] = p->tiles.get();
     arrays[1] = p->ops.data();
@@ -837,6 +953,41 @@ extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[8])
     arrays[5] = p->halves.data();
     arrays[6] = p->stage_bounds[0].data();
     arrays[7] = p->stage_bounds[1].data();
+    arrays[8] = p->rec.data();
+    arrays[9] = p->xpos.data();
+    return 0;
+}
+
+extern "C" int bfsht_rec_coeffs(int64_t m, int64_t k_max, double *out) {
+    if (!out || m < 0) return -1;
+    for (int64_t k = m; k < k_max; ++k) bfr_coeffs(m, k, &out[2 * (k - m)], &out[2 * (k - m) + 1]);
+    return 0;
+}
+
+// Host twin of the engine's tile generation (engine.cu regen_tile).
+extern "C" int bfsht_regen_tile_host(const double *seed, int R, int C, const double *rec,
+                                     const double *x_pos, double mag_min, double *out) {
+    if (!seed || !rec || !x_pos || !out || R < 1 || R > BF_T || C < 1 || C > BF_T) return -1;
+    int32_t hdr[2];
+    std::memcpy(hdr, seed, sizeof(hdr));
+    int64_t rb;
+    std::memcpy(&rb, seed + 1, sizeof(rb));
+    const int C4 = (C + 3) / 4;
+    std::memset(out, 0, sizeof(double) * bf_tile_doubles(R, C));
+    for (int r = 0; r < R; ++r) {
+        double pp = seed[2 + 3 * r], pc = seed[3 + 3 * r];
+        int e = (int)seed[4 + 3 * r];
+        const double xr = x_pos[hdr[0] + r];
+        for (int c = 0; c < C; ++c) {
+            double v = std::ldexp(pc, e);
+            if (std::fabs(v) < mag_min) v = 0.0;
+            out[bf_tile_index(r, c, C4)] = v;
+            if (c + 1 < C) {
+                bfr_step(xr, rec[rb + 4 * c], rec[rb + 4 * c + 1], &pp, &pc, &e);
+                bfr_step(xr, rec[rb + 4 * c + 2], rec[rb + 4 * c + 3], &pp, &pc, &e);
+            }
+        }
+    }
     return 0;
 }
 

@@ -20,9 +20,12 @@
 #include <math.h>
 #include <stdint.h>
 
-#define BFSHT_BIG 0x1p500
-#define BFSHT_SMALL 0x1p-500
-#define BFSHT_RESCALE 1000
+#include "recur.h"
+
+static inline double emit(double p_cur, int e, double mag_min) {
+    double v = ldexp(p_cur, e);
+    return fabs(v) < mag_min ? 0.0 : v;
+}
 
 /* out is row-major n x ncols; degrees m + offset + 2j, j < ncols. */
 int bfsht_legendre_half_table(int64_t m, int64_t offset, int64_t n,
@@ -41,33 +44,13 @@ int bfsht_legendre_half_table(int64_t m, int64_t offset, int64_t n,
         double *row = out + r * ncols;
         int64_t j = 0;
         if (k_first == m) {
-            double v = ldexp(p_cur, e);
-            if (fabs(v) < mag_min) v = 0.0;
-            row[j++] = v;
+            row[j++] = emit(p_cur, e, mag_min);
         }
         for (int64_t k = m; k < k_last; ++k) {
             const int64_t s = k - m;
-            const double t1 = xr * p_cur;
-            const double t2 = alpha[s] * t1;
-            const double t3 = beta[s] * p_prev;
-            const double p_next = t2 - t3;
-            p_prev = p_cur;
-            p_cur = p_next;
-            const double a = fabs(p_cur), b = fabs(p_prev);
-            const double mx = a > b ? a : b;
-            if (mx > BFSHT_BIG) {
-                p_cur = ldexp(p_cur, -BFSHT_RESCALE);
-                p_prev = ldexp(p_prev, -BFSHT_RESCALE);
-                e += BFSHT_RESCALE;
-            } else if (mx < BFSHT_SMALL && mx > 0.0) {
-                p_cur = ldexp(p_cur, BFSHT_RESCALE);
-                p_prev = ldexp(p_prev, BFSHT_RESCALE);
-                e -= BFSHT_RESCALE;
-            }
+            bfr_step(xr, alpha[s], beta[s], &p_prev, &p_cur, &e);
             if (j < ncols && k + 1 == k_first + 2 * j) {
-                double v = ldexp(p_cur, e);
-                if (fabs(v) < mag_min) v = 0.0;
-                row[j++] = v;
+                row[j++] = emit(p_cur, e, mag_min);
             }
         }
     }
@@ -90,33 +73,13 @@ int bfsht_legendre_table(int64_t m, int64_t npts, const double *x,
         double *row = out + r * ndeg;
         int64_t d = 0;
         if (degrees[0] == m) {
-            double v = ldexp(p_cur, e);
-            if (fabs(v) < mag_min) v = 0.0;
-            row[d++] = v;
+            row[d++] = emit(p_cur, e, mag_min);
         }
         for (int64_t k = m; k < k_stop; ++k) {
             const int64_t s = k - m;
-            const double t1 = xr * p_cur;
-            const double t2 = alpha[s] * t1;
-            const double t3 = beta[s] * p_prev;
-            const double p_next = t2 - t3;
-            p_prev = p_cur;
-            p_cur = p_next;
-            const double a = fabs(p_cur), b = fabs(p_prev);
-            const double mx = a > b ? a : b;
-            if (mx > BFSHT_BIG) {
-                p_cur = ldexp(p_cur, -BFSHT_RESCALE);
-                p_prev = ldexp(p_prev, -BFSHT_RESCALE);
-                e += BFSHT_RESCALE;
-            } else if (mx < BFSHT_SMALL && mx > 0.0) {
-                p_cur = ldexp(p_cur, BFSHT_RESCALE);
-                p_prev = ldexp(p_prev, BFSHT_RESCALE);
-                e -= BFSHT_RESCALE;
-            }
+            bfr_step(xr, alpha[s], beta[s], &p_prev, &p_cur, &e);
             if (d < ndeg && degrees[d] == k + 1) {
-                double v = ldexp(p_cur, e);
-                if (fabs(v) < mag_min) v = 0.0;
-                row[d++] = v;
+                row[d++] = emit(p_cur, e, mag_min);
             }
         }
     }

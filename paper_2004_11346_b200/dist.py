@@ -126,6 +126,13 @@ class _Common:
         entries = int(h["ncols"][present].sum()) + int(present.sum()) * self.n
         return 8 * self.dp.packed.stats["payload_values"] + 32 * entries
 
+    def hbm_bytes(self):
+        """Bytes the ALT stages actually stream per direction: like
+        alt_bytes, but regenerated tiles count their seed blocks instead
+        of their values (B_ALT with and without them)."""
+        pk = self.dp.packed
+        return self.alt_bytes() - 8 * pk.stats["regen_values"] + pk.seed_bytes()
+
     def time_alt(self, reps=3):
         import torch
         out = {}
@@ -237,7 +244,7 @@ class ShardedSht(_Common):
     [r0, r1): rows n-r1..n-r0-1 then n+r0..n+r1-1.
     """
 
-    def __init__(self, n, plans, orders, rank, world, group=None):
+    def __init__(self, n, plans, orders, rank, world, group=None, regen=0.0):
         import torch
         import torch.distributed as dist
         from .api import DevicePlan
@@ -246,7 +253,7 @@ class ShardedSht(_Common):
         self.group = group
         self.orders = list(orders)
         self.dp = DevicePlan(plans, weights=plans[0].quadrature.weights
-                             if plans else None)
+                             if plans else None, regen=regen)
         lib = self.dp.lib
         self.lib = lib
         dev = self.dp.device

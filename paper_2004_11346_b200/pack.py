@@ -29,7 +29,9 @@ class BlockDesc(ctypes.Structure):
 
 class Manifest(ctypes.Structure):
     _fields_ = [("n", _I32), ("norders", _I32), ("m", _P), ("ncols", _P),
-                ("nblocks", _I64), ("blocks", _P)]
+                ("nblocks", _I64), ("blocks", _P), ("regen", ctypes.c_double),
+                ("x_pos", _P), ("mant0", _P), ("exp0", _P),
+                ("mag_min", ctypes.c_double)]
 
 
 def declare(lib):
@@ -40,6 +42,11 @@ def declare(lib):
     lib.bfsht_packed_info.argtypes = [_P, ctypes.POINTER(_I64)]
     lib.bfsht_packed_arrays.restype = ctypes.c_int
     lib.bfsht_packed_arrays.argtypes = [_P, ctypes.POINTER(_P)]
+    lib.bfsht_rec_coeffs.restype = ctypes.c_int
+    lib.bfsht_rec_coeffs.argtypes = [_I64, _I64, _P]
+    lib.bfsht_regen_tile_host.restype = ctypes.c_int
+    lib.bfsht_regen_tile_host.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P,
+                                          ctypes.c_double, _P]
     lib.bfsht_packed_free.restype = None
     lib.bfsht_packed_free.argtypes = [_P]
     lib.bfsht_host_last_error.restype = ctypes.c_char_p
@@ -58,7 +65,8 @@ NRHS = 4
 INFO_KEYS = ("tile_doubles", "ops", "idx", "maps", "tasks", "arena",
              "halves", "stages_fwd", "stages_inv", "payload_values",
              "yr", "butterfly_blocks", "lowrank_blocks",
-             "dense_blocks", "n", "norders", "free_fwd", "free_inv")
+             "dense_blocks", "n", "norders", "free_fwd", "free_inv",
+             "regen_tiles", "regen_values", "rec_doubles", "xpos_doubles")
 INFO_LEN = 24
 
 
@@ -76,7 +84,7 @@ class PackedPlan:
         lib.bfsht_packed_info(handle, info)
         self.info = np.array(list(info), dtype=np.int64)
         self.stats = dict(zip(INFO_KEYS, (int(v) for v in self.info)))
-        arr = (_P * 8)()
+        arr = (_P * 10)()
         lib.bfsht_packed_arrays(handle, arr)
         s = self.stats
 
@@ -95,6 +103,29 @@ class PackedPlan:
         self.halves = view(5, HALF_DTYPE, s["halves"])
         self.stages_fwd = view(6, np.int64, s["stages_fwd"] + 1)
         self.stages_inv = view(7, np.int64, s["stages_inv"] + 1)
+        self.rec = view(8, np.float64, s["rec_doubles"])
+        self.xpos = view(9, np.float64, s["xpos_doubles"])
+        self.mag_min = float(self.info[22:23].view(np.float64)[0])
+
+    @property
+    def regen_tiles(self):
+        return self.stats["regen_tiles"]
+
+    def stored_payload_values(self):
+        """Reference values that cross HBM (regenerated tiles excluded)."""
+        return self.stats["payload_values"] - self.stats["regen_values"]
+
+    def seed_bytes(self):
+        """Bytes of the regeneration seed blocks (read instead of values)."""
+        return 8 * self._seed_doubles()
+
+    def _seed_doubles(self):
+        sel = (self.ops["flags"] & 4) != 0
+        if not sel.any():
+            return 0
+        tiles, first = np.unique(self.ops["tile"][sel], return_index=True)
+        rows = self.ops["R"][sel][first].astype(np.int64)
+        return int(np.sum((2 + 3 * rows + 15) // 16 * 16))
 
     @property
     def n(self):
@@ -128,8 +159,11 @@ def _kind_of(payload):
     return 2
 
 
-def pack_plans(plans, n=None, threads=0):
-    """Pack AltPlans (all at the same half-size N) into the device format."""
+def pack_plans(plans, n=None, threads=0, regen=0.0):
+    """Pack AltPlans (all at the same half-size N) into the device format.
+
+    regen in [0, 1]: fraction of the full-height dense turning tiles stored
+    as recurrence seeds and regenerated on the GPU."""
     plans = list(plans)
     if not plans and n is None:
         raise ValueError("nothing to pack")
@@ -192,6 +226,18 @@ def pack_plans(plans, n=None, threads=0):
     arr = (BlockDesc * max(len(descs), 1))(*descs)
     man = Manifest(n=n, norders=len(plans), m=_addr(ms), ncols=_addr(ncols),
                    nblocks=len(descs), blocks=ctypes.cast(arr, _P))
+    if regen > 0.0 and plans:
+        from .legendre import MAG_MIN, start_values
+        spec = plans[0].spec_odd if plans[0].spec_odd is not None else plans[0].spec_even
+        x_pos = np.ascontiguousarray(spec.x_pos, dtype=np.float64)
+        mant0 = np.empty((len(plans), n), dtype=np.float64)
+        exp0 = np.empty((len(plans), n), dtype=np.int32)
+        for o, plan in enumerate(plans):
+            mant0[o], exp0[o] = start_values(plan.m, x_pos)
+        keep += [x_pos, mant0, exp0]
+        man.regen = float(regen)
+        man.x_pos, man.mant0, man.exp0 = _addr(x_pos), _addr(mant0), _addr(exp0)
+        man.mag_min = MAG_MIN
     lib = native.host()
     out = _P()
     rc = lib.bfsht_pack_plan(ctypes.byref(man), int(threads), ctypes.byref(out))

@@ -9,7 +9,7 @@ import numpy as np
 from paper_2004_11346_b200.pack import NRHS
 
 OP_N, OP_T, OP_ADD = 0, 1, 2
-F_GATHER, F_LANEMAP = 1, 2
+F_GATHER, F_LANEMAP, F_REGEN = 1, 2, 4
 SLOTS = 64   # outputs per task (format.h BF_SLOTS)
 
 
@@ -19,6 +19,23 @@ def tile_matrix(pk, off, R, C):
     r = np.arange(R)[:, None]
     c = np.arange(C)[None, :]
     return pk.tiles[off + ((r >> 2) * c4 + (c >> 2)) * 16 + (r & 3) * 4 + (c & 3)]
+
+
+def regen_matrix(pk, off, R, C):
+    """R x C values of a regenerated tile, through the host twin of the
+    engine's generation (bfsht_regen_tile_host)."""
+    import ctypes
+    from paper_2004_11346_b200 import native
+    lib = native.host()
+    c4 = (C + 3) // 4
+    buf = np.zeros(((R + 3) // 4) * c4 * 16)
+    seed = pk.tiles[off:]
+    rc = lib.bfsht_regen_tile_host(seed.ctypes.data, R, C, pk.rec.ctypes.data,
+                                   pk.xpos.ctypes.data, pk.mag_min, buf.ctypes.data)
+    assert rc == 0
+    r = np.arange(R)[:, None]
+    c = np.arange(C)[None, :]
+    return buf[((r >> 2) * c4 + (c >> 2)) * 16 + (r & 3) * 4 + (c & 3)]
 
 
 def run_direction(pk, arena, direction):
@@ -35,7 +52,10 @@ def run_direction(pk, arena, direction):
                         if src >= 0:
                             acc[off + j] += arena[src]
                     continue
-                a = tile_matrix(pk, int(op["tile"]), R, C)
+                if op["flags"] & F_REGEN:
+                    a = regen_matrix(pk, int(op["tile"]), R, C)
+                else:
+                    a = tile_matrix(pk, int(op["tile"]), R, C)
                 nin = C if kind == OP_N else R
                 src = pk.idx[op["in"]:op["in"] + nin] if gather \
                     else np.arange(op["in"], op["in"] + nin)
