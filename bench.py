@@ -146,6 +146,20 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def measured_traffic(n, world, regen):
+    """DRAM bytes (read + write) per direction of the ALT stages from the
+    committed ncu launch list of this command (profiles/), for the same
+    workload only; None otherwise."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{n}.json")) as fh:
+            t = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    if world != 1 or regen > 0 or t.get("n") != n:
+        return None
+    return t["traffic_bytes_per_direction"]
+
+
 # ----------------------------------------------------------- reference arm
 _REF_STATE = {}
 
@@ -362,7 +376,8 @@ def run_ours(args):
     alt_ms = 0.5 * (alt["fwd_ms"] + alt["inv_ms"])
     achieved = alt_bytes_all / world / (alt_ms * 1e-3) / 1e9  # per GPU
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "unit": "GB/s", "frac": achieved / peak,
+                "traffic": measured_traffic(n, world, args.regen),
                 "kernel": "alt_stage_kernel (all ALT stages of one direction)",
                 "alt_fwd_ms": alt["fwd_ms"], "alt_inv_ms": alt["inv_ms"],
                 "alg_bytes_per_direction": alt_bytes_all / world,

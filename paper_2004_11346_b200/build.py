@@ -70,9 +70,10 @@ def build_cuda(force=False):
     objs = []
     for src in srcs:
         obj = os.path.join(CSRC, os.path.basename(src) + ".o")
+        extra = os.environ.get("BFSHT_NVCC_FLAGS", "").split()
         _run([NVCC] + ARCH + ["-O3", "-lineinfo", "-std=c++17",
                               "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-                              "-I", INCLUDE, "-I", CSRC, "-c", src, "-o", obj])
+                              "-I", INCLUDE, "-I", CSRC] + extra + ["-c", src, "-o", obj])
         objs.append(obj)
     # the packer rides along so C users get pack + upload + apply in one .so
     pk = os.path.join(CSRC, "packer.cpp")
