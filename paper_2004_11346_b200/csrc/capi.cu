@@ -52,6 +52,11 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
             li[h].x = 1;
         }
         pl->host_halves.assign(host_halves, host_halves + nh);
+        std::vector<int> ny(nh ? nh : 1, -1);
+        for (int64_t h = 0; h < nh; ++h) ny[h] = host_halves[h].ncols > 0 ? host_halves[h].y : -1;
+        BF_CUDA(cudaMalloc(&pl->node_y, sizeof(int) * ny.size()));
+        pl->owned.push_back(pl->node_y);
+        BF_CUDA(cudaMemcpy(pl->node_y, ny.data(), sizeof(int) * ny.size(), cudaMemcpyHostToDevice));
         pl->host_layout_fwd = lf;
         BF_CUDA(cudaMalloc(&pl->layout_fwd, sizeof(bf_half) * (nh ? nh : 1)));
         pl->owned.push_back(pl->layout_fwd);
@@ -118,6 +123,12 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
         return -2;
     }
     pl->owned.push_back(arena);
+    // zeroed: absent halves' entries of the node array Yr are read as zeros
+    if (cudaMemset(arena, 0, (size_t)pl->info[5] * BF_NRHS * 8 + 16) != cudaSuccess) {
+        g_err = "arena clear failed";
+        bfsht_plan_free(pl);
+        return -2;
+    }
     pl->tiles = (const double *)dev[0];
     pl->ops = (const bf_op *)dev[1];
     pl->idx = (const int32_t *)dev[2];

@@ -24,6 +24,7 @@ struct bfsht_plan {
     bf_half *layout_fwd = nullptr;
     bf_half *layout_inv = nullptr;
     std::vector<bf_half> host_halves, host_layout_fwd;   // host copies
+    int *node_y = nullptr;            // device: node-half base per half, -1 absent
     double *arena = nullptr;
     std::vector<int64_t> stages[2];   // task bounds per stage (host)
     int32_t n = 0;                    // half size N

@@ -192,7 +192,11 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
-    double2 *scratch, bool w_smem) {
+    double2 *scratch, bool w_smem, int64_t yr, int ystride) {
+    // ystride > 0 (whole-SHT path): entry (order am, parity p, row rr) sits
+    // at yr + rr * ystride + 2 am + p in the row-major node array Yr, and
+    // absent halves read as zeros there (never written), so no layout-table
+    // lookup stands between a bin and its loads.  Otherwise:
     // node-half entries of row pair r live at halves[.].y + (r - r_begin);
     // grid holds 2*r_count local rows: lower rows n-r_begin-r_count .. n-r_begin-1
     // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
@@ -215,6 +219,26 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     // otherwise a chain of dependent DRAM latencies per bin)
     constexpr int kBatch = 8;
     for (int b0 = threadIdx.x; b0 < L; b0 += kBatch * blockDim.x) {
+        double2 go[kBatch], ge[kBatch], t[kBatch];
+        int p[kBatch];
+        if (ystride > 0) {
+            const double *rowp = arena + (yr + (int64_t)rr * ystride) * BF_NRHS;
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) {
+                const int b = b0 + i * blockDim.x;
+                const bool ok = b < L;
+                const int m = ok ? (b <= mtop ? b : b - L) : 0;
+                const int am = m < 0 ? -m : m;
+                const int sel = (ok && b > mtop) ? 2 : 0;
+                go[i] = ge[i] = make_double2(0.0, 0.0);
+                if (ok) {
+                    go[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am) * BF_NRHS + sel);
+                    ge[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * BF_NRHS + sel);
+                }
+                t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
+                p[i] = ok ? perm[b] : 0;
+            }
+        } else {
         bf_half ho[kBatch], he[kBatch];
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
@@ -224,8 +248,6 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
             ho[i] = halves[2 * am];
             he[i] = halves[2 * am + 1];
         }
-        double2 go[kBatch], ge[kBatch], t[kBatch];
-        int p[kBatch];
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
             const int b = b0 + i * blockDim.x;
@@ -240,6 +262,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
                     arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * BF_NRHS + sel);
             t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
             p[i] = ok ? perm[b] : 0;
+        }
         }
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
@@ -268,7 +291,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
     const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
-    double2 *scratch, bool w_smem) {
+    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny) {
     const int L = d.L;
     double2 *buf = dft_buffer<SM>(scratch, 2, L);
     // twiddle table next to the rows in shared memory when it fits
@@ -276,9 +299,16 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     if (SM && w_smem) {
         double2 *ws = buf + 2 * L;
         for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
-        __syncthreads();
         Wt = ws;
     }
+    // whole-SHT path: node-half bases (-1 = absent half) staged in shared
+    // memory after the twiddles, replacing per-bin layout-table loads
+    int *ys = nullptr;
+    if (SM && w_smem && node_y) {
+        ys = reinterpret_cast<int *>(buf + 3 * L);
+        for (int i = threadIdx.x; i < ny; i += blockDim.x) ys[i] = node_y[i];
+    }
+    __syncthreads();
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
     const double2 *up = grid + (int64_t)(r_count + rr) * L;
@@ -316,8 +346,18 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
             const int b = b0 + i * blockDim.x;
             const int m = b < L ? (b <= mtop ? b : b - L) : 0;
             const int am = m < 0 ? -m : m;
-            ho[i] = halves[2 * am];
-            he[i] = halves[2 * am + 1];
+            if (ys) {
+                const int yo = ys[2 * am], ye = ys[2 * am + 1];
+                ho[i].y = yo;
+                ho[i].x = 1;
+                ho[i].ncols = yo >= 0;
+                he[i].y = ye;
+                he[i].x = 1;
+                he[i].ncols = ye >= 0;
+            } else {
+                ho[i] = halves[2 * am];
+                he[i] = halves[2 * am + 1];
+            }
             t[i] = b < L ? tw[b] : make_double2(0.0, 0.0);
         }
 #pragma unroll
@@ -487,6 +527,13 @@ int dft_smem_bytes(int64_t L, int rows) { return (int)(rows * L * 16); }
 // two rows + the twiddle table when that fits the 227 KB opt-in limit
 bool dft_w_smem(int64_t L) { return 3 * L * 16 <= 227 * 1024; }
 int dft_pair_smem(int64_t L) { return dft_smem_bytes(L, dft_w_smem(L) ? 3 : 2); }
+// analysis kernel: + node-half bases (int32 per half) when they fit too
+bool dft_y_smem(int64_t L, int64_t nh) {
+    return dft_w_smem(L) && 3 * L * 16 + 4 * nh <= 227 * 1024;
+}
+int dft_anal_smem(int64_t L, int64_t nh) {
+    return dft_pair_smem(L) + (dft_y_smem(L, nh) ? (int)(4 * nh) : 0);
+}
 
 }  // namespace
 
@@ -541,7 +588,8 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     } else {
         const int pair = dft_pair_smem(L);
         BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
-        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
+        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     std::max(pair, dft_anal_smem(L, 2 * (int64_t)pl->norders))));
         BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
     }
     return 0;
@@ -568,7 +616,8 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), pl->info[10],
+        2 * pl->norders);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -582,10 +631,13 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    const int64_t nh = 2 * (int64_t)pl->norders;
+    const bool ysm = sm && dft_y_smem(pl->dft_L, nh);
+    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(pl->dft_L, nh) : dft_pair_smem(pl->dft_L)) : 0, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
+        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L),
+        ysm ? pl->node_y : nullptr, (int)nh);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
@@ -810,8 +862,8 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
+        reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), (int64_t)0, 0);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -829,7 +881,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L));
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), nullptr, 0);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
