@@ -96,6 +96,8 @@ class DevicePlan:
                 up(pk.halves.view(np.int32)),
                 up(pk.rec if pk.rec.size else np.zeros(2)),
                 up(pk.xpos if pk.xpos.size else np.zeros(2)),
+                up(pk.flow if pk.flow.size else np.zeros(1, np.int32)),
+                up(pk.tinfo if pk.tinfo.size else np.zeros(1, np.int32)),
             ]
             self.arena = torch.zeros((max(pk.stats["arena"], 1), NRHS),
                                      dtype=torch.float64, device=self.device)
@@ -112,12 +114,15 @@ class DevicePlan:
             host[5] = self._host_halves.ctypes.data
             host[6] = self._sf.ctypes.data
             host[7] = self._si.ctypes.data
-            dev = (ctypes.c_void_p * 10)()
+            dev = (ctypes.c_void_p * 12)()
             for i, t in enumerate(self._dev[:6]):
                 dev[i] = t.data_ptr()
             dev[6] = self.arena.data_ptr()
             dev[7] = self._dev[6].data_ptr()
             dev[8] = self._dev[7].data_ptr()
+            if pk.flow.size:
+                dev[9] = self._dev[8].data_ptr()
+                dev[10] = self._dev[9].data_ptr()
             h = ctypes.c_void_p()
             check(self.lib, self.lib.bfsht_plan_wrap(info, host, dev,
                                                      ctypes.byref(h)),
@@ -135,6 +140,12 @@ class DevicePlan:
 
     def launches(self):
         return int(self.lib.bfsht_plan_launches(self.handle))
+
+    def set_schedule(self, dataflow=True):
+        """ALT schedule: dataflow (one persistent launch per direction) or
+        one launch per stage (the default); results are bitwise identical."""
+        check(self.lib, self.lib.bfsht_plan_schedule(self.handle, 1 if dataflow else 0),
+              "bfsht_plan_schedule")
 
     # -------------------------------------------------------------- apply
     def alt_apply(self, direction, stream=None):

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -69,6 +70,23 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
                                cudaMemcpyHostToDevice));
         }
     }
+    if (pl->flow && pl->tinfo && pl->info[23] > 0) {
+        const size_t nc = 2 * (BFSHT_MAX_FLOW_STAGES + 1);
+        BF_CUDA(cudaMalloc(&pl->flow_ctr, sizeof(int) * nc));
+        pl->owned.push_back(pl->flow_ctr);
+        BF_CUDA(cudaMemset(pl->flow_ctr, 0, sizeof(int) * nc));
+        std::vector<int> need(2 * BFSHT_MAX_FLOW_STAGES, 0);
+        for (int d = 0; d < 2; ++d)
+            for (size_t s = 0; s + 1 < pl->stages[d].size() && s < BFSHT_MAX_FLOW_STAGES; ++s)
+                need[d * BFSHT_MAX_FLOW_STAGES + s] = (int)(pl->stages[d][s + 1] - pl->stages[d][s]);
+        BF_CUDA(cudaMalloc(&pl->flow_need, sizeof(int) * need.size()));
+        pl->owned.push_back(pl->flow_need);
+        BF_CUDA(cudaMemcpy(pl->flow_need, need.data(), sizeof(int) * need.size(),
+                           cudaMemcpyHostToDevice));
+    } else {
+        pl->flow = nullptr;
+        pl->tinfo = nullptr;
+    }
     pl->ncounters = (int)std::max(pl->info[7], pl->info[8]) + 1;
     BF_CUDA(cudaMalloc(&pl->counters, sizeof(int) * pl->ncounters));
     pl->owned.push_back(pl->counters);
@@ -95,17 +113,19 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
         g_err = "bad packed plan";
         return -1;
     }
-    const void *arr[10];
+    const void *arr[12];
     bfsht_packed_arrays(p, arr);
-    // device copies of arrays 0..5 and 8..9 (stage bounds stay on the host)
-    const int which[8] = {0, 1, 2, 3, 4, 5, 8, 9};
-    const size_t sz[8] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
-                          (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
-                          (size_t)pl->info[4] * sizeof(bf_task),
-                          (size_t)pl->info[6] * sizeof(bf_half),
-                          (size_t)pl->info[20] * 8, (size_t)pl->info[21] * 8};
-    void *dev[8];
-    for (int i = 0; i < 8; ++i) {
+    // device copies of arrays 0..5 and 8..11 (stage bounds stay on the host)
+    const int which[10] = {0, 1, 2, 3, 4, 5, 8, 9, 10, 11};
+    const size_t sz[10] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
+                           (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
+                           (size_t)pl->info[4] * sizeof(bf_task),
+                           (size_t)pl->info[6] * sizeof(bf_half),
+                           (size_t)pl->info[20] * 8, (size_t)pl->info[21] * 8,
+                           (size_t)pl->info[23] * 4,
+                           (size_t)(pl->info[23] > 0 ? pl->info[4] : 0) * 4};
+    void *dev[10];
+    for (int i = 0; i < 10; ++i) {
         dev[i] = nullptr;
         if (cudaMalloc(&dev[i], sz[i] ? sz[i] : 16) != cudaSuccess ||
             (sz[i] && cudaMemcpy(dev[i], arr[which[i]], sz[i], cudaMemcpyHostToDevice) != cudaSuccess)) {
@@ -137,6 +157,8 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     pl->halves = (const bf_half *)dev[5];
     pl->rec = (const double *)dev[6];
     pl->xpos = (const double *)dev[7];
+    pl->flow = (const int32_t *)dev[8];
+    pl->tinfo = (const int32_t *)dev[9];
     pl->arena = (double *)arena;
     int rc = finish_plan(pl, (const bf_half *)arr[5], (const int64_t *)arr[6],
                          (const int64_t *)arr[7]);
@@ -149,7 +171,7 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
 }
 
 int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
-                    void *const dev[10], bfsht_plan **out) {
+                    void *const dev[12], bfsht_plan **out) {
     if (!info || !host || !dev || !out) {
         g_err = "null argument";
         return -1;
@@ -165,6 +187,8 @@ int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8
     pl->arena = (double *)dev[6];
     pl->rec = (const double *)dev[7];
     pl->xpos = (const double *)dev[8];
+    pl->flow = (const int32_t *)dev[9];
+    pl->tinfo = (const int32_t *)dev[10];
     if (info[18] > 0 && (!pl->rec || !pl->xpos)) {
         delete pl;
         g_err = "plan has regenerated tiles but no coefficient table / nodes";
@@ -193,6 +217,12 @@ void bfsht_plan_free(bfsht_plan *pl) {
 }
 
 double *bfsht_plan_arena(bfsht_plan *pl) { return pl ? pl->arena : nullptr; }
+
+int bfsht_plan_schedule(bfsht_plan *pl, int dataflow) {
+    if (!pl) return -1;
+    pl->dataflow = dataflow != 0;
+    return 0;
+}
 
 int bfsht_plan_tune(bfsht_plan *pl, int overlap, int chain_ctas) {
     if (!pl) return -1;

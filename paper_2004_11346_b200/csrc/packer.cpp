@@ -68,6 +68,10 @@ struct bfsht_packed {
     std::vector<double> rec;            // per order: (alpha, beta) for s = 0 .. 2N-m-1
     std::vector<double> xpos;
     double mag_min = 0.0;
+    // dataflow schedule (one launch per direction): claim order per
+    // direction (fwd then inv) and per task stage | (dep stage + 1) << 8
+    std::vector<int32_t> flow;
+    std::vector<int32_t> tinfo;
 };
 
 namespace {
@@ -371,6 +375,100 @@ struct Packer {
                 inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, C,
                                                    (int)(cc.first - (int64_t)gc * BF_T), flags));
             }
+    }
+
+    // Dataflow schedule.  Every task gets its stage and the stage it depends
+    // on (the nearest non-empty earlier stage; -1 for none): butterfly /
+    // low-rank chain stages depend on their predecessor; a final group task
+    // depends on the chain only if one of its ops reads a chain output —
+    // "pure" group tasks (dense or low-rank-second-half tiles reading only
+    // the direction's inputs: forward coefficient halves, inverse node
+    // halves) depend on nothing; combine tasks depend on the group stage.
+    // The claim order interleaves the pure group tasks into the chain: each
+    // chain stage is spread over a share of them and followed by a gap of
+    // pure tasks long enough for the stage to finish before the next one is
+    // claimed, so no warp idles at a stage boundary and the latency-bound
+    // chain runs under the HBM-bound dense stream.  Every task with
+    // dependency d comes after all tasks of stage d in the order (no warp can
+    // wait on a task claimed after its own).
+    void build_flow(int G) {
+        P.tinfo.assign(P.tasks.size(), 0);
+        P.flow.clear();
+        if (P.free_stage[0] >= 0 || P.free_stage[1] >= 0) return;   // split schedule: staged only
+        const char *gap_env = std::getenv("BFSHT_FLOW_GAP");
+        const int64_t gap_tasks = gap_env ? std::atoll(gap_env) : 2 * 148 * 12;
+        for (int d = 0; d < 2; ++d) {
+            const auto &b = P.stage_bounds[d];
+            const int nst = (int)b.size() - 1;
+            const size_t f0 = P.flow.size();
+            std::vector<std::pair<int64_t, int64_t>> iv;
+            for (const bf_half &hf : P.halves)
+                if (hf.ncols > 0)
+                    iv.push_back(d == 0 ? std::make_pair((int64_t)hf.x, (int64_t)hf.x + hf.ncols)
+                                        : std::make_pair((int64_t)hf.y, (int64_t)hf.y + M.n));
+            std::sort(iv.begin(), iv.end());
+            auto is_input = [&](int64_t e) {
+                auto it = std::upper_bound(iv.begin(), iv.end(), std::make_pair(e, INT64_MAX));
+                if (it == iv.begin()) return false;
+                --it;
+                return e >= it->first && e < it->second;
+            };
+            auto pure = [&](const bf_task &t) {
+                for (int32_t i = 0; i < t.op_count; ++i) {
+                    const bf_op &o = P.ops[t.op_begin + i];
+                    if (o.kind == BF_OP_ADD || (o.flags & BF_OPF_GATHER)) return false;
+                    const int nvec = o.kind == BF_OP_TILE_N ? o.C : o.R;
+                    if (!is_input(o.in) || !is_input((int64_t)o.in + nvec - 1)) return false;
+                }
+                return true;
+            };
+            auto prev_nonempty = [&](int s) {
+                for (int q = s - 1; q >= 0; --q)
+                    if (b[q + 1] > b[q]) return q;
+                return -1;
+            };
+            std::vector<int32_t> pure_ids, mixed_ids, tail_ids;
+            std::vector<int> chain;
+            for (int s = 0; s < nst; ++s) {
+                if (s < G && b[s + 1] > b[s]) chain.push_back(s);
+                for (int64_t t = b[s]; t < b[s + 1]; ++t) {
+                    int dep = prev_nonempty(s);
+                    if (s == G) {
+                        if (pure(P.tasks[t])) {
+                            dep = -1;
+                            pure_ids.push_back((int32_t)t);
+                        } else {
+                            mixed_ids.push_back((int32_t)t);
+                        }
+                    } else if (s > G) {
+                        tail_ids.push_back((int32_t)t);
+                    }
+                    P.tinfo[t] = s | ((dep + 1) << 8);
+                }
+            }
+            const int64_t np = (int64_t)pure_ids.size();
+            const int64_t K = (int64_t)chain.size();
+            int64_t pi = 0;
+            for (int64_t j = 0; j < K; ++j) {
+                const int s = chain[j];
+                const int64_t budget = np * (j + 1) / (K + 1) - np * j / (K + 1);
+                const int64_t gap = std::min(budget, gap_tasks);
+                const int64_t mix = budget - gap;
+                const int64_t ns = b[s + 1] - b[s];
+                int64_t emitted = 0;
+                for (int64_t i = 0; i < ns; ++i) {
+                    P.flow.push_back((int32_t)(b[s] + i));
+                    const int64_t want = mix * (i + 1) / ns;
+                    for (; emitted < want; ++emitted) P.flow.push_back(pure_ids[pi++]);
+                }
+                for (int64_t g = 0; g < gap; ++g) P.flow.push_back(pure_ids[pi++]);
+            }
+            while (pi < np) P.flow.push_back(pure_ids[pi++]);
+            P.flow.insert(P.flow.end(), mixed_ids.begin(), mixed_ids.end());
+            P.flow.insert(P.flow.end(), tail_ids.begin(), tail_ids.end());
+            if ((int64_t)(P.flow.size() - f0) != b[nst] - b[0])
+                throw std::runtime_error("dataflow order is not a permutation of the tasks");
+        }
     }
 
     // Recurrence-coefficient tables and per-row seeds of the regenerated
@@ -872,6 +970,7 @@ struct Packer {
                 P.stage_bounds[d].push_back((int64_t)P.tasks.size());
             }
         }
+        build_flow(last);
         // fill tiles
         const int64_t nj = (int64_t)jobs.size();
         P.tiles.reset(new double[(size_t)std::max<int64_t>(P.n_tiles, 2)]);
@@ -937,13 +1036,15 @@ extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_
     info[20] = (int64_t)p->rec.size();
     info[21] = (int64_t)p->xpos.size();
     std::memcpy(&info[22], &p->mag_min, sizeof(double));
+    info[23] = (int64_t)p->flow.size();
     return 0;
 }
 
 // arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves,
 //         6 stage bounds fwd (int64, stages+1), 7 stage bounds inv,
-//         8 recurrence coefficients, 9 x_pos
-extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[10]) {
+//         8 recurrence coefficients, 9 x_pos, 10 dataflow order (fwd
+//         then inv task ids), 11 per-task stage | (dep + 1) << 8
+extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]) {
     if (!p) return -1;
     arrays[0] = p->tiles.get();
     arrays[1] = p->ops.data();
@@ -955,6 +1056,8 @@ extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[10]
     arrays[7] = p->stage_bounds[1].data();
     arrays[8] = p->rec.data();
     arrays[9] = p->xpos.data();
+    arrays[10] = p->flow.data();
+    arrays[11] = p->tinfo.data();
     return 0;
 }
 

@@ -84,7 +84,7 @@ class PackedPlan:
         lib.bfsht_packed_info(handle, info)
         self.info = np.array(list(info), dtype=np.int64)
         self.stats = dict(zip(INFO_KEYS, (int(v) for v in self.info)))
-        arr = (_P * 10)()
+        arr = (_P * 12)()
         lib.bfsht_packed_arrays(handle, arr)
         s = self.stats
 
@@ -105,6 +105,9 @@ class PackedPlan:
         self.stages_inv = view(7, np.int64, s["stages_inv"] + 1)
         self.rec = view(8, np.float64, s["rec_doubles"])
         self.xpos = view(9, np.float64, s["xpos_doubles"])
+        nflow = int(self.info[23])
+        self.flow = view(10, np.int32, nflow)
+        self.tinfo = view(11, np.int32, s["tasks"] if nflow else 0)
         self.mag_min = float(self.info[22:23].view(np.float64)[0])
 
     @property
