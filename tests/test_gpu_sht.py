@@ -51,3 +51,22 @@ def test_sht_matches_oracle_and_dense(n):
     back = sht_inverse(plan, got).pack()
     assert rel(back, OA.sht_inverse(plan.alt_plans, n, got)) < 1e-12
     assert rel(back, flat) < 1e-12
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_real_grid_inverse_tol_1e10(n):
+    # config C5 semantics: a real grid (iid U(-1,1)) into sht_inverse is
+    # promoted to complex (sht.py:151-166); plans at tolerance 1e-10 (C3/C5)
+    from paper_2004_11346_b200 import SamplingConfig
+    from paper_2004_11346_b200.api import sht_inverse
+    plan = plan_sht(n, SamplingConfig(tolerance=1e-10))
+    rng = np.random.default_rng(n)
+    grid = rng.uniform(-1.0, 1.0, (2 * n, 4 * n - 1))
+    got = sht_inverse(plan, grid).pack()
+    want = OA.sht_inverse(plan.alt_plans, n, grid.astype(np.complex128))
+    assert rel(got, want) < 1e-12
+    # (1+k)^-2 spectrum forward (C5 forward input) round trip
+    flat = random_flat(n, n + 1, decay=2)
+    from paper_2004_11346_b200.api import sht_forward
+    g = sht_forward(plan, ShtCoeffs.unpack(n, flat)).values
+    assert rel(g, OA.sht_forward(plan.alt_plans, n, flat)) < 1e-12
