@@ -154,6 +154,80 @@ class PackedPlan:
             pass
 
 
+# ------------------------------------------------------------- plan cache
+# Packed plans on disk ("compact device-plan cache"): the
+# packed arrays exactly as uploaded, each 4 KB aligned so a load is a set of
+# read-only memory maps that DevicePlan uploads without another host copy.
+# Planning N=1024 takes seconds here but the reference needs minutes (hours
+# at N=4096); a cached plan skips planning and packing entirely.
+_PK_MAGIC = b"BFPK"
+_PK_VERSION = 1
+_PK_ALIGN = 4096
+_PK_FIELDS = ("tiles", "ops", "idx", "maps", "tasks", "halves", "stages_fwd",
+              "stages_inv", "rec", "xpos", "flow", "tinfo")
+
+
+def save_packed(pk, path):
+    """Write a PackedPlan (or a loaded one) to `path`."""
+    import struct
+    arrays = [np.ascontiguousarray(getattr(pk, f)) for f in _PK_FIELDS]
+    head = _PK_MAGIC + struct.pack("<II", _PK_VERSION, len(arrays))
+    head += np.asarray(pk.info, dtype="<i8").tobytes()
+    offs, pos = [], _PK_ALIGN
+    for a in arrays:
+        offs.append(pos)
+        pos += -(-a.nbytes // _PK_ALIGN) * _PK_ALIGN
+    head += np.asarray([[o, a.nbytes] for o, a in zip(offs, arrays)], dtype="<i8").tobytes()
+    if len(head) > _PK_ALIGN:
+        raise ValueError("plan cache header too large")
+    with open(path, "wb") as fh:
+        fh.write(head.ljust(_PK_ALIGN, b"\0"))
+        for o, a in zip(offs, arrays):
+            fh.seek(o)
+            fh.write(memoryview(a).cast("B"))
+        fh.truncate(pos)
+
+
+class LoadedPlan:
+    """A packed plan memory-mapped from a cache file: the PackedPlan
+    attributes DevicePlan and the tests read."""
+
+    def __init__(self, path):
+        import struct
+        with open(path, "rb") as fh:
+            head = fh.read(_PK_ALIGN)
+        if head[:4] != _PK_MAGIC:
+            raise ValueError(f"{path}: not a packed-plan file")
+        ver, count = struct.unpack("<II", head[4:12])
+        if ver != _PK_VERSION or count != len(_PK_FIELDS):
+            raise ValueError(f"{path}: unsupported packed-plan version {ver}")
+        self.info = np.frombuffer(head, dtype="<i8", count=INFO_LEN, offset=12).copy()
+        self.stats = dict(zip(INFO_KEYS, (int(v) for v in self.info)))
+        tab = np.frombuffer(head, dtype="<i8", count=2 * count, offset=12 + 8 * INFO_LEN)
+        dtypes = (np.float64, OP_DTYPE, np.int32, np.int8, TASK_DTYPE, HALF_DTYPE,
+                  np.int64, np.int64, np.float64, np.float64, np.int32, np.int32)
+        for f, dt, (off, nb) in zip(_PK_FIELDS, dtypes, tab.reshape(-1, 2)):
+            dt = np.dtype(dt)
+            if nb == 0:
+                setattr(self, f, np.zeros(0, dtype=dt))
+            else:
+                setattr(self, f, np.memmap(path, dtype=dt, mode="r", offset=int(off),
+                                           shape=(int(nb) // dt.itemsize,)))
+        self.mag_min = float(self.info[22:23].view(np.float64)[0])
+
+    n = PackedPlan.n
+    orders = PackedPlan.orders
+    payload_bytes = PackedPlan.payload_bytes
+    regen_tiles = PackedPlan.regen_tiles
+    stored_payload_values = PackedPlan.stored_payload_values
+    seed_bytes = PackedPlan.seed_bytes
+    _seed_doubles = PackedPlan._seed_doubles
+
+
+def load_packed(path):
+    return LoadedPlan(path)
+
+
 def _kind_of(payload):
     if hasattr(payload, "factors"):
         return 0
