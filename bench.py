@@ -62,6 +62,9 @@ def parse():
                     help="c2: SHT fwd+inv (default, the headline); c4: batched "
                          "forward ALT of 64 fields (wide DMMA engine)")
     ap.add_argument("--fields", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=1,
+                    help="C2 with B <= 4 independent transforms per step sharing one "
+                         "payload pass (16-RHS engine); default 1 = the single transform")
     ap.add_argument("--regen", type=float, default=0.0,
                     help="fraction of full-height dense turning tiles regenerated "
                          "on the GPU from recurrence seeds (SURVEY f1)")
@@ -287,6 +290,8 @@ def cpu_baseline_single(plans, n, flat):
 
 def run_ours(args):
     import torch
+    if args.batch < 1 or args.batch > 4:
+        raise SystemExit("--batch must be 1..4")
     from paper_2004_11346_b200 import SamplingConfig, plan_orders
     from paper_2004_11346_b200.api import ShtDevice, DevicePlan
     from paper_2004_11346_b200 import dist as D
@@ -294,6 +299,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.batch > 1:
+        raise SystemExit("--batch > 1 is single-GPU only")
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -316,7 +323,7 @@ def run_ours(args):
         eng = ShtDevice.__new__(ShtDevice)
         eng.n = n
         eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights, regen=args.regen)
-        runner = D.SingleRunner(eng)
+        runner = D.SingleRunner(eng, batch=args.batch)
     else:
         runner = D.ShardedSht(n, plans, orders, rank, world, regen=args.regen)
     torch.cuda.synchronize()
@@ -357,7 +364,7 @@ def run_ours(args):
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    value = 1e3 / ms
+    value = 1e3 / ms * args.batch
 
     # ------------------------------------- roofline: ALT stage, device events
     alt = runner.time_alt(reps=3)
@@ -402,7 +409,7 @@ def run_ours(args):
         e2e["ms"] = float(t.item())
     # the host output of the last timed step must be the input back
     want = torch.from_numpy(np.ascontiguousarray(
-        runner.shard_coeffs(flat) if world > 1 else flat))
+        runner.shard_coeffs(flat) if world > 1 else runner.host_coeffs(flat)))
     got = runner.last_e2e_output
     t = torch.tensor([float(torch.linalg.norm(got - want)) ** 2,
                       float(torch.linalg.norm(want)) ** 2], device=dev, dtype=torch.float64)
@@ -413,7 +420,7 @@ def run_ours(args):
     check = None
     if args.check and world == 1:
         import oracle.apply as OA
-        g = grid.cpu().numpy()
+        g = (grid[0] if args.batch > 1 else grid).cpu().numpy()
         want = OA.sht_forward(plans, n, flat)
         check = float(np.linalg.norm(g - want) / np.linalg.norm(want))
 
@@ -432,7 +439,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C2: SHT fwd+inv N={n}, tol {args.tol:g}",
+            "config": {"workload": f"C2: SHT fwd+inv N={n}, tol {args.tol:g}"
+                                   + (f", {args.batch} independent transforms per step"
+                                      if args.batch > 1 else ""),
+                       "batch": args.batch,
                        "n": n, "tol": args.tol, "n0": 512,
                        "grid": [2 * n, 4 * n - 1],
                        "payload_values_rank0": int(payload_values),
@@ -440,7 +450,7 @@ def run_ours(args):
                        "parallelism": f"orders sharded over {world} GPU(s)"},
             "roofline": roofline,
             "cpu_baseline": cpu,
-            "e2e": {"value": 1e3 / e2e["ms"], "unit": UNIT,
+            "e2e": {"value": 1e3 / e2e["ms"] * args.batch, "unit": UNIT,
                     "h2d_bytes_per_step": e2e["h2d"], "d2h_bytes_per_step": e2e["d2h"],
                     "api": "api.HostPipeline (pinned host buffers; copies on "
                            "their own streams overlap other steps' transforms)",

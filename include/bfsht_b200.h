@@ -171,6 +171,18 @@ int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
 int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, double *out,
                      const double *weights, double *work, void *stream);
 
+/* Batched SHT: `batch` (1..4) independent transforms in one pass of the
+ * 16-RHS engine over the payload (each stored value read once for all of
+ * them; transform b owns doubles [4b, 4b+4) of every wide entry).  FORWARD:
+ * in = batch x 4N^2 coefficients (ShtCoeffs.pack() order each), out = batch
+ * x 2N x (4N-1) grids; INVERSE the reverse (weights required).  Outputs are
+ * bitwise those of `batch` bfsht_sht_forward / _inverse calls. */
+int bfsht_sht_batch(bfsht_plan *pl, int dir, int batch, const double *in, double *out,
+                    const double *weights, double *work, void *stream);
+/* All ALT stages of one direction over a wide (BFSHT_WIDE_NRHS) arena with
+ * inputs already in place (profiling / timing of the batched paths). */
+int bfsht_alt_apply_wide(bfsht_plan *pl, int dir, double *work, void *stream);
+
 /* Raw half apply: the matrix of one (order, parity) half — for a plan built
  * from a single ButterflyFactorization, exactly idbf_apply (FORWARD, K x) /
  * idbf_apply_transpose (INVERSE, K^T y) (butterfly.py:275-292).  in/out are

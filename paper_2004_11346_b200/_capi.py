@@ -31,6 +31,10 @@ def declare(lib):
     lib.bfsht_alt_orders.argtypes = [_P, _I, _P, _P, _P, _P]
     lib.bfsht_alt_fields.restype = _I
     lib.bfsht_alt_fields.argtypes = [_P, _I, _I, _P, _P, _P, _P, _P]
+    lib.bfsht_alt_apply_wide.restype = _I
+    lib.bfsht_alt_apply_wide.argtypes = [_P, _I, _P, _P]
+    lib.bfsht_sht_batch.restype = _I
+    lib.bfsht_sht_batch.argtypes = [_P, _I, _I, _P, _P, _P, _P, _P]
     lib.bfsht_half_apply.restype = _I
     lib.bfsht_half_apply.argtypes = [_P, _I, _I, _I, _P, _P, _P, _P]
     lib.bfsht_sht_forward.restype = _I
@@ -64,7 +68,8 @@ EXPORTS = (
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena", "bfsht_plan_tune",
     "bfsht_plan_schedule",
     "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_alt_fields",
-    "bfsht_half_apply", "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
+    "bfsht_half_apply", "bfsht_sht_batch", "bfsht_alt_apply_wide",
+    "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
     "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",
     "bfsht_gather_entries", "bfsht_scatter_entries", "bfsht_synth_rows",
     "bfsht_anal_rows",

@@ -154,6 +154,13 @@ class DevicePlan:
         check(self.lib, self.lib.bfsht_alt_apply(
             self.handle, direction, _stream_ptr(torch, stream)), "bfsht_alt_apply")
 
+    def alt_apply_wide(self, direction, stream=None):
+        """All ALT stages over the wide (16-RHS) arena, inputs in place."""
+        torch = _torch()
+        check(self.lib, self.lib.bfsht_alt_apply_wide(
+            self.handle, direction, ctypes.c_void_p(self.wide_arena().data_ptr()),
+            _stream_ptr(torch, stream)), "bfsht_alt_apply_wide")
+
     def alt_orders(self, direction, inp, out=None, stream=None):
         """Per-order ALT on device complex128 tensors laid out plan after
         plan: forward in = coefficients (2N-m each), out = 2N node values;
@@ -198,6 +205,25 @@ class DevicePlan:
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
             ctypes.c_void_p(self.wide_arena().data_ptr()),
             _stream_ptr(torch, stream)), "bfsht_alt_fields")
+        return out
+
+    def sht_batch(self, direction, inp, out=None, stream=None):
+        """B <= 4 independent whole transforms in one payload pass.
+        FORWARD: inp (B, 4N^2) coefficients -> (B, 2N, 4N-1) grids;
+        INVERSE: grids -> coefficients.  Bitwise equal to B single calls."""
+        torch = _torch()
+        n = self.n
+        inp = inp.contiguous()
+        nb = inp.shape[0]
+        if out is None:
+            shape = (nb, 2 * n, 4 * n - 1) if direction == FORWARD else (nb, 4 * n * n)
+            out = torch.empty(shape, dtype=torch.complex128, device=self.device)
+        w = self.weights.data_ptr() if self.weights is not None else None
+        check(self.lib, self.lib.bfsht_sht_batch(
+            self.handle, direction, int(nb), ctypes.c_void_p(inp.data_ptr()),
+            ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
+            ctypes.c_void_p(self.wide_arena().data_ptr()),
+            _stream_ptr(torch, stream)), "bfsht_sht_batch")
         return out
 
     def half_apply(self, direction, half, x, stream=None):
@@ -417,6 +443,14 @@ class ShtDevice:
 
     def inverse(self, grid, out=None, stream=None):
         return self.plan.sht_inverse(grid, out, stream)
+
+    def forward_batch(self, coeffs, out=None, stream=None):
+        """(B, 4N^2) device coefficients, B <= 4 -> (B, 2N, 4N-1) grids."""
+        return self.plan.sht_batch(FORWARD, coeffs, out, stream)
+
+    def inverse_batch(self, grids, out=None, stream=None):
+        """(B, 2N, 4N-1) device grids, B <= 4 -> (B, 4N^2) coefficients."""
+        return self.plan.sht_batch(INVERSE, grids, out, stream)
 
     def pipeline(self, depth=3):
         """Host-buffer streaming handle (see HostPipeline)."""

@@ -322,6 +322,33 @@ static int check_sht(bfsht_plan *pl) {
     return 0;
 }
 
+int bfsht_alt_apply_wide(bfsht_plan *pl, int dir, double *work, void *stream) {
+    if (!pl || !work || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan, direction or work arena";
+        return -1;
+    }
+    return bf_alt_apply_wide(pl, dir, work, (cudaStream_t)stream);
+}
+
+int bfsht_sht_batch(bfsht_plan *pl, int dir, int batch, const double *in, double *out,
+                    const double *weights, double *work, void *stream) {
+    int rc = check_sht(pl);
+    if (rc) return rc;
+    if (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE) {
+        g_err = "bad direction";
+        return -1;
+    }
+    if (batch < 1 || batch > BFSHT_WIDE_NRHS / 4 || !in || !out || !work) {
+        g_err = "batch must be 1..4 with device buffers and a wide work arena";
+        return -1;
+    }
+    if (dir == BFSHT_INVERSE && !weights) {
+        g_err = "inverse SHT needs quadrature weights";
+        return -1;
+    }
+    return bf_sht_batch(pl, dir, batch, in, out, weights, work, (cudaStream_t)stream);
+}
+
 int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, void *stream) {
     if (check_sht(pl)) return -1;
 

@@ -79,6 +79,8 @@ int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
 int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);
 int bf_alt_fields(bfsht_plan *pl, int dir, int F, const double *in, double *out,
                   const double *weights, double *work, cudaStream_t st);
+int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
+                 const double *weights, double *work, cudaStream_t st);
 int bf_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
                   double *work, cudaStream_t st);
 // sht.cu

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
-    double2 *scratch, bool w_smem, int64_t yr, int ystride) {
+    double2 *scratch, bool w_smem, int64_t yr, int ystride, int ew) {
     // ystride > 0 (whole-SHT path): entry (order am, parity p, row rr) sits
     // at yr + rr * ystride + 2 am + p in the row-major node array Yr, and
     // absent halves read as zeros there (never written), so no layout-table
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         double2 go[kBatch], ge[kBatch], t[kBatch];
         int p[kBatch];
         if (ystride > 0) {
-            const double *rowp = arena + (yr + (int64_t)rr * ystride) * BF_NRHS;
+            const double *rowp = arena + (yr + (int64_t)rr * ystride) * ew;
 #pragma unroll
             for (int i = 0; i < kBatch; ++i) {
                 const int b = b0 + i * blockDim.x;
@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
                 const int sel = (ok && b > mtop) ? 2 : 0;
                 go[i] = ge[i] = make_double2(0.0, 0.0);
                 if (ok) {
-                    go[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am) * BF_NRHS + sel);
-                    ge[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * BF_NRHS + sel);
+                    go[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am) * ew + sel);
+                    ge[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew + sel);
                 }
                 t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
                 p[i] = ok ? perm[b] : 0;
@@ -256,10 +256,10 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
             go[i] = ge[i] = make_double2(0.0, 0.0);
             if (ok && ho[i].ncols > 0)
                 go[i] = *reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * BF_NRHS + sel);
+                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew + sel);
             if (ok && he[i].ncols > 0)
                 ge[i] = *reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * BF_NRHS + sel);
+                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew + sel);
             t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
             p[i] = ok ? perm[b] : 0;
         }
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
     const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
-    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny) {
+    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny, int ew) {
     const int L = d.L;
     double2 *buf = dft_buffer<SM>(scratch, 2, L);
     // twiddle table next to the rows in shared memory when it fits
@@ -371,13 +371,13 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
             sa = cmul(make_double2(sa.x * invL, sa.y * invL), tc);
             sb = cmul(make_double2(sb.x * invL, sb.y * invL), tc);
             if (ho[i].ncols > 0) {
-                double *e = arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * BF_NRHS;
+                double *e = arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew;
                 *reinterpret_cast<double2 *>(e + sel) =
                     make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
                 if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
             }
             if (he[i].ncols > 0) {
-                double *e = arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * BF_NRHS;
+                double *e = arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew;
                 *reinterpret_cast<double2 *>(e + sel) =
                     make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
                 if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
@@ -396,7 +396,7 @@ __device__ __forceinline__ int64_t coeff_offset(int m, int K) {
 
 // coefficient halves for the whole SHT: entry = (Re, Im) of +m then -m
 __global__ void coef_pack_kernel(int n, const bf_half *__restrict__ halves,
-                                 const double2 *__restrict__ c, double *__restrict__ arena) {
+                                 const double2 *__restrict__ c, double *__restrict__ arena, int ew) {
     const int am = blockIdx.y;
     const int K = 2 * n;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -404,16 +404,16 @@ __global__ void coef_pack_kernel(int n, const bf_half *__restrict__ halves,
         const bf_half h = halves[2 * am + par];
         if (j >= h.ncols) continue;
         const int k = (par == 0 ? 1 : 0) + 2 * j;
-        const double2 p = c[coeff_offset(am, K) + k];
-        const double2 q = am ? c[coeff_offset(-am, K) + k] : make_double2(0.0, 0.0);
-        double *e = arena + ((int64_t)h.x + j) * BF_NRHS;
+        const double2 p = c ? c[coeff_offset(am, K) + k] : make_double2(0.0, 0.0);
+        const double2 q = (c && am) ? c[coeff_offset(-am, K) + k] : make_double2(0.0, 0.0);
+        double *e = arena + ((int64_t)h.x + j) * ew;
         *reinterpret_cast<double2 *>(e) = p;
         *reinterpret_cast<double2 *>(e + 2) = q;
     }
 }
 
 __global__ void coef_unpack_kernel(int n, const bf_half *__restrict__ halves,
-                                   const double *__restrict__ arena, double2 *__restrict__ c) {
+                                   const double *__restrict__ arena, double2 *__restrict__ c, int ew) {
     const int am = blockIdx.y;
     const int K = 2 * n;
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -421,7 +421,7 @@ __global__ void coef_unpack_kernel(int n, const bf_half *__restrict__ halves,
         const bf_half h = halves[2 * am + par];
         if (j >= h.ncols) continue;
         const int k = (par == 0 ? 1 : 0) + 2 * j;
-        const double *e = arena + ((int64_t)h.x + j) * BF_NRHS;
+        const double *e = arena + ((int64_t)h.x + j) * ew;
         c[coeff_offset(am, K) + k] = *reinterpret_cast<const double2 *>(e);
         if (am) c[coeff_offset(-am, K) + k] = *reinterpret_cast<const double2 *>(e + 2);
     }
@@ -605,7 +605,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     if (rc) return rc;
     dim3 g1((n + 255) / 256, 2 * n);
     coef_pack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, reinterpret_cast<const double2 *>(coeffs),
-                                         pl->arena);
+                                         pl->arena, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_FORWARD, st);
@@ -617,7 +617,7 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), pl->info[10],
-        2 * pl->norders);
+        2 * pl->norders, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -637,14 +637,14 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
         weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L),
-        ysm ? pl->node_y : nullptr, (int)nh);
+        ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
     if (rc) return rc;
     dim3 g1((n + 255) / 256, 2 * n);
     coef_unpack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, pl->arena,
-                                           reinterpret_cast<double2 *>(coeffs));
+                                           reinterpret_cast<double2 *>(coeffs), BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -834,6 +834,69 @@ int bf_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, do
     return 0;
 }
 
+// Batched SHT: B <= BF_WIDE_NRHS / BF_NRHS independent transforms share one
+// pass of the 16-RHS engine over the payload; transform b owns doubles
+// [4b, 4b + 4) of every wide arena entry, so packing, the DFT stage and
+// unpacking are the single-transform kernels with entry width 16 and an
+// offset.  Outputs are bitwise those of B single-transform calls.
+int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
+                 const double *weights, double *work, cudaStream_t st) {
+    const int n = pl->n;
+    const int ew = BF_WIDE_NRHS;
+    int rc = bf_dft_prepare(pl, 4LL * n - 1);
+    if (rc) return rc;
+    const int64_t L = pl->dft_L;
+    const int64_t ncoef = 4LL * n * n, ngrid = 2LL * n * L;
+    const bool sm = pl->dft_scratch == nullptr;
+    const DftDesc d = make_desc(pl);
+    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
+    dim3 g1((n + 255) / 256, 2 * n);
+    if (dir == BFSHT_FORWARD) {
+        for (int b = 0; b < ew / BF_NRHS; ++b) {
+            const double2 *src = b < B ? reinterpret_cast<const double2 *>(in) + b * ncoef : nullptr;
+            coef_pack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, src, work + BF_NRHS * b, ew);
+            BF_CUDA(cudaGetLastError());
+            pl->launches += 1;
+        }
+        rc = bf_alt_apply_wide(pl, BFSHT_FORWARD, work, st);
+        if (rc) return rc;
+        for (int b = 0; b < B; ++b) {
+            (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(L) : 0, st>>>(
+                d, n, pl->layout_fwd, work + BF_NRHS * b, 0, n,
+                reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+                reinterpret_cast<const double2 *>(pl->dft_w),
+                reinterpret_cast<double2 *>(out) + b * ngrid, sm,
+                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L), pl->info[10],
+                2 * pl->norders, ew);
+            BF_CUDA(cudaGetLastError());
+            pl->launches += 1;
+        }
+    } else {
+        const int64_t nh = 2 * (int64_t)pl->norders;
+        const bool ysm = sm && dft_y_smem(L, nh);
+        for (int b = 0; b < B; ++b) {
+            (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(L, nh) : dft_pair_smem(L)) : 0, st>>>(
+                d, n, pl->layout_inv, work + BF_NRHS * b,
+                reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
+                reinterpret_cast<const double2 *>(pl->dft_w),
+                reinterpret_cast<const double2 *>(in) + b * ngrid, weights, 0, n, sm,
+                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L),
+                ysm ? pl->node_y : nullptr, (int)nh, ew);
+            BF_CUDA(cudaGetLastError());
+            pl->launches += 1;
+        }
+        rc = bf_alt_apply_wide(pl, BFSHT_INVERSE, work, st);
+        if (rc) return rc;
+        for (int b = 0; b < B; ++b) {
+            coef_unpack_kernel<<<g1, 256, 0, st>>>(n, pl->halves, work + BF_NRHS * b,
+                                                   reinterpret_cast<double2 *>(out) + b * ncoef, ew);
+            BF_CUDA(cudaGetLastError());
+            pl->launches += 1;
+        }
+    }
+    return 0;
+}
+
 int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *in, double *out,
                 cudaStream_t st) {
     int rc = bf_dft_prepare(pl, L);
@@ -863,7 +926,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), (int64_t)0, 0);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), (int64_t)0, 0, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -881,7 +944,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), nullptr, 0);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), nullptr, 0, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;

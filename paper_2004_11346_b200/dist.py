@@ -163,8 +163,10 @@ class _Common:
         from .api import HostPipeline
         c, g, _ = self.make_buffers(flat)
         coeff_shape, grid_shape = tuple(c.shape), tuple(g.shape)
-        host0 = torch.from_numpy(np.ascontiguousarray(
-            flat if not hasattr(self, "shard_coeffs") else self.shard_coeffs(flat)))
+        if hasattr(self, "shard_coeffs"):
+            host0 = torch.from_numpy(np.ascontiguousarray(self.shard_coeffs(flat)))
+        else:
+            host0 = torch.from_numpy(np.ascontiguousarray(self.host_coeffs(flat)))
         nbuf = lag + 2
         h_c = [host0.clone().pin_memory() for _ in range(nbuf)]
         h_g = [torch.empty(grid_shape, dtype=torch.complex128).pin_memory()
@@ -210,25 +212,69 @@ class _Common:
 class SingleRunner(_Common):
     """Whole SHT on one GPU (plan holds every order)."""
 
-    def __init__(self, sht_device):
+    def __init__(self, sht_device, batch=1):
         self.dev = sht_device
         self.dp = sht_device.plan
         self.n = sht_device.n
+        self.batch = int(batch)
         self._pinned = None
 
     def make_buffers(self, flat):
+        """Device coefficients / grid / result; with batch B > 1 the same
+        coefficient set is stacked B times (independent transforms)."""
         import torch
         dev = self.dp.device
         n = self.n
         c = torch.from_numpy(np.ascontiguousarray(flat)).to(dev)
-        g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128, device=dev)
+        if self.batch > 1:
+            c = c.unsqueeze(0).repeat(self.batch, 1).contiguous()
+            g = torch.empty((self.batch, 2 * n, 4 * n - 1), dtype=torch.complex128, device=dev)
+        else:
+            g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128, device=dev)
         return c, g, torch.empty_like(c)
 
+    def host_coeffs(self, flat):
+        if self.batch > 1:
+            return np.ascontiguousarray(np.broadcast_to(flat, (self.batch, flat.size)))
+        return flat
+
     def forward(self, coeffs, grid):
-        self.dp.sht_forward(coeffs, grid)
+        if self.batch > 1:
+            self.dp.sht_batch(FORWARD, coeffs, grid)
+        else:
+            self.dp.sht_forward(coeffs, grid)
 
     def inverse(self, grid, coeffs):
-        self.dp.sht_inverse(grid, coeffs)
+        if self.batch > 1:
+            self.dp.sht_batch(INVERSE, grid, coeffs)
+        else:
+            self.dp.sht_inverse(grid, coeffs)
+
+    def alt_bytes(self):
+        if self.batch == 1:
+            return _Common.alt_bytes(self)
+        h = self.dp.packed.halves
+        present = h["ncols"] > 0
+        entries = int(h["ncols"][present].sum()) + int(present.sum()) * self.n
+        return 8 * self.dp.packed.stats["payload_values"] + 128 * entries
+
+    def time_alt(self, reps=3):
+        if self.batch == 1:
+            return _Common.time_alt(self, reps)
+        import torch
+        out = {}
+        for name, d in (("fwd_ms", FORWARD), ("inv_ms", INVERSE)):
+            self.dp.alt_apply_wide(d)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(reps):
+                self.dp.alt_apply_wide(d)
+            e1.record()
+            torch.cuda.synchronize()
+            out[name] = e0.elapsed_time(e1) / reps
+        return out
 
     def roundtrip_error(self, coeffs, grid, back):
         self.forward(coeffs, grid)
