@@ -37,7 +37,15 @@ struct DftDesc {
     int L;
     int nrad;
     int radix[kMaxRadix];
+    // per pass: exact multiplicative inverse of the pass's span (the product
+    // of the earlier radices), x / span == __umulhi(x, span_inv) for every
+    // butterfly index x < L (checked on the host when the table is built)
+    unsigned span_inv[kMaxRadix];
 };
+
+__device__ __forceinline__ int fast_div(int x, unsigned inv) {
+    return inv ? (int)__umulhi((unsigned)x, inv) : x;   // inv 0: span 1
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -54,7 +62,7 @@ __device__ __forceinline__ double2 conjif(double2 a, bool c) {
 // naive size-P DFT.
 template <int P>
 __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int span,
-                                           const double2 *W, bool inv) {
+                                           unsigned span_inv, const double2 *W, bool inv) {
     double cr[P], ci[P];
 #pragma unroll
     for (int t = 0; t < P; ++t) {
@@ -65,8 +73,9 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
     const int nb = L / P;
     const int tstep = L / (span * P);
     for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
-        const int rw = t / nb, tt = t - rw * nb;
-        const int k = tt % span, g = tt / span;
+        // nrows <= 2: the row by one compare, the group by a multiply-high
+        const int rw = t >= nb ? 1 : 0, tt = t - rw * nb;
+        const int g = fast_div(tt, span_inv), k = tt - g * span;
         double2 *row = buf + (int64_t)rw * L;
         const int base = g * span * P + k;
         double2 x[P];
@@ -137,13 +146,14 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d,
     int span = 1;
     for (int ri = 0; ri < d.nrad; ++ri) {
         const int P = d.radix[ri];
+        const unsigned si = d.span_inv[ri];
         switch (P) {
-            case 2: radix_pass<2>(buf, nrows, L, span, W, inv); break;
-            case 3: radix_pass<3>(buf, nrows, L, span, W, inv); break;
-            case 5: radix_pass<5>(buf, nrows, L, span, W, inv); break;
-            case 7: radix_pass<7>(buf, nrows, L, span, W, inv); break;
-            case 11: radix_pass<11>(buf, nrows, L, span, W, inv); break;
-            case 13: radix_pass<13>(buf, nrows, L, span, W, inv); break;
+            case 2: radix_pass<2>(buf, nrows, L, span, si, W, inv); break;
+            case 3: radix_pass<3>(buf, nrows, L, span, si, W, inv); break;
+            case 5: radix_pass<5>(buf, nrows, L, span, si, W, inv); break;
+            case 7: radix_pass<7>(buf, nrows, L, span, si, W, inv); break;
+            case 11: radix_pass<11>(buf, nrows, L, span, si, W, inv); break;
+            case 13: radix_pass<13>(buf, nrows, L, span, si, W, inv); break;
             default: {
                 const int nb = L / P;
                 for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
@@ -518,7 +528,14 @@ DftDesc make_desc(const bfsht_plan *pl) {
     DftDesc d;
     d.L = (int)pl->dft_L;
     d.nrad = (int)pl->dft_radix.size();
-    for (int i = 0; i < d.nrad; ++i) d.radix[i] = pl->dft_radix[i];
+    int64_t span = 1;
+    for (int i = 0; i < d.nrad; ++i) {
+        d.radix[i] = pl->dft_radix[i];
+        // ceil(2^32 / span): exact for the quotients used (x < L <= 2^20,
+        // verified exhaustively in bf_dft_prepare)
+        d.span_inv[i] = span == 1 ? 0u : (unsigned)(((1ULL << 32) + span - 1) / span);
+        span *= pl->dft_radix[i];
+    }
     return d;
 }
 
@@ -543,6 +560,22 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     if ((int)rad.size() > kMaxRadix) {
         bfsht_set_error("DFT length has too many prime factors");
         return -4;
+    }
+    {
+        // the multiply-high quotients of make_desc must be exact for every
+        // butterfly index of every pass
+        int64_t span = 1;
+        for (int p : rad) {
+            if (span > 1) {
+                const uint64_t inv = ((1ULL << 32) + span - 1) / span;
+                for (int64_t x = 0; x < L; ++x)
+                    if ((int64_t)(((uint64_t)x * inv) >> 32) != x / span) {
+                        bfsht_set_error("DFT index division check failed");
+                        return -4;
+                    }
+            }
+            span *= p;
+        }
     }
     for (int p : rad)
         if (p > 128) {
