@@ -149,7 +149,7 @@ class _Common:
             out[name] = e0.elapsed_time(e1) / reps
         return out
 
-    def time_e2e(self, flat, steps, warmup, barrier, lag=2, depth=3):
+    def time_e2e(self, flat, steps, warmup, barrier, lag=3, depth=4):
         """Host API end to end: pinned host coefficients -> host grid ->
         host coefficients for every step, through api.HostPipeline (copies
         on their own streams, overlapped with other steps' transforms).
