@@ -46,7 +46,7 @@ struct bfsht_plan {
     int64_t *order_off = nullptr;     // device, 2*norders+2 offsets
     // DFT tables (built lazily for L = 4N-1)
     int64_t dft_L = 0;
-    double *dft_w = nullptr;          // L complex: exp(-2 pi i k / L)
+    double *dft_w = nullptr;          // pass twiddle table (L complex) + radix roots
     int32_t *dft_perm = nullptr;      // digit-reversal positions
     double *dft_tw = nullptr;         // L complex: exp(i m phi0) per bin
     std::vector<int32_t> dft_radix;

@@ -41,6 +41,11 @@ struct DftDesc {
     // of the earlier radices), x / span == __umulhi(x, span_inv) for every
     // butterfly index x < L (checked on the host when the table is built)
     unsigned span_inv[kMaxRadix];
+    // per pass: offset of its twiddle block in the pass table (entries
+    // (q-1) * span + k, contiguous in the butterfly index k, so a warp's
+    // twiddle loads are consecutive) and of its P radix roots
+    int tw_off[kMaxRadix];
+    int root_off[kMaxRadix];
 };
 
 __device__ __forceinline__ int fast_div(int x, unsigned inv) {
@@ -55,23 +60,28 @@ __device__ __forceinline__ double2 conjif(double2 a, bool c) {
 }
 
 // One radix-P pass over all butterflies of `nrows` rows (whole CTA).
-// Radix roots are loaded once per pass into registers.  Odd P uses the
-// conjugate-pair form: with a_j = x_j + x_{P-j}, b_j = x_j - x_{P-j},
+// Radix roots are loaded once per pass into registers; the inter-pass
+// twiddles come from the pass table Tw (entry (q-1)*span + k = W^{q k L/(span P)},
+// the value the flat root table held at q*k*tstep), which keeps a warp's
+// twiddle loads on consecutive addresses (no shared-memory bank
+// conflicts); the first pass (span 1) has only unit twiddles and skips
+// them.  Odd P uses the conjugate-pair form: with a_j = x_j + x_{P-j},
+// b_j = x_j - x_{P-j},
 //   y_s, y_{P-s} = x_0 + sum_j a_j cos(2 pi js/P)  +/-  i sum_j b_j sin(..)
 // (signs per direction), about a quarter of the P^2 complex products of a
 // naive size-P DFT.
 template <int P>
 __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int span,
-                                           unsigned span_inv, const double2 *W, bool inv) {
+                                           unsigned span_inv, const double2 *Tw,
+                                           const double2 *__restrict__ R, bool inv) {
     double cr[P], ci[P];
 #pragma unroll
     for (int t = 0; t < P; ++t) {
-        const double2 w = W[t * (L / P)];
+        const double2 w = R[t];
         cr[t] = w.x;
         ci[t] = inv ? -w.y : w.y;
     }
     const int nb = L / P;
-    const int tstep = L / (span * P);
     for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
         // nrows <= 2: the row by one compare, the group by a multiply-high
         const int rw = t >= nb ? 1 : 0, tt = t - rw * nb;
@@ -80,9 +90,10 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
         const int base = g * span * P + k;
         double2 x[P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) {
-            x[q] = row[base + q * span];
-            if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
+        for (int q = 0; q < P; ++q) x[q] = row[base + q * span];
+        if (span > 1) {
+#pragma unroll
+            for (int q = 1; q < P; ++q) x[q] = cmul(x[q], conjif(Tw[(q - 1) * span + k], inv));
         }
         if (P == 2) {
             row[base] = make_double2(x[0].x + x[1].x, x[0].y + x[1].y);
@@ -119,19 +130,17 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
 }
 
 // generic radix (large primes), local-memory arrays
-__device__ void butterfly_any(double2 *row, int base, int span, int k, int L, int P,
-                              const double2 *__restrict__ W, bool inv) {
+__device__ void butterfly_any(double2 *row, int base, int span, int k, int P, const double2 *Tw,
+                              const double2 *__restrict__ R, bool inv) {
     double2 x[128];
-    const int tstep = L / (span * P);
-    const int rstep = L / P;
     for (int q = 0; q < P; ++q) {
         x[q] = row[base + q * span];
-        if (q > 0) x[q] = cmul(x[q], conjif(W[q * k * tstep], inv));
+        if (q > 0 && span > 1) x[q] = cmul(x[q], conjif(Tw[(q - 1) * span + k], inv));
     }
     for (int s = 0; s < P; ++s) {
         double2 acc = x[0];
         for (int q = 1; q < P; ++q) {
-            double2 t = cmul(x[q], conjif(W[((q * s) % P) * rstep], inv));
+            double2 t = cmul(x[q], conjif(R[(q * s) % P], inv));
             acc.x += t.x;
             acc.y += t.y;
         }
@@ -139,27 +148,30 @@ __device__ void butterfly_any(double2 *row, int base, int span, int k, int L, in
     }
 }
 
-// All passes over `nrows` rows of buf (row stride L), whole CTA.
-__device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d,
-                           const double2 *__restrict__ W, bool inv) {
+// All passes over `nrows` rows of buf (row stride L), whole CTA.  Tw: the
+// pass twiddle table (L entries, shared or global memory); R: radix roots.
+__device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const double2 *Tw,
+                           const double2 *__restrict__ R, bool inv) {
     const int L = d.L;
     int span = 1;
     for (int ri = 0; ri < d.nrad; ++ri) {
         const int P = d.radix[ri];
         const unsigned si = d.span_inv[ri];
+        const double2 *tw = Tw + d.tw_off[ri];
+        const double2 *rr = R + d.root_off[ri];
         switch (P) {
-            case 2: radix_pass<2>(buf, nrows, L, span, si, W, inv); break;
-            case 3: radix_pass<3>(buf, nrows, L, span, si, W, inv); break;
-            case 5: radix_pass<5>(buf, nrows, L, span, si, W, inv); break;
-            case 7: radix_pass<7>(buf, nrows, L, span, si, W, inv); break;
-            case 11: radix_pass<11>(buf, nrows, L, span, si, W, inv); break;
-            case 13: radix_pass<13>(buf, nrows, L, span, si, W, inv); break;
+            case 2: radix_pass<2>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 3: radix_pass<3>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 5: radix_pass<5>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 7: radix_pass<7>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 11: radix_pass<11>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 13: radix_pass<13>(buf, nrows, L, span, si, tw, rr, inv); break;
             default: {
                 const int nb = L / P;
                 for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
                     const int rw = t / nb, tt = t - rw * nb;
                     const int k = tt % span, g = tt / span;
-                    butterfly_any(buf + (int64_t)rw * L, g * span * P + k, span, k, L, P, W, inv);
+                    butterfly_any(buf + (int64_t)rw * L, g * span * P + k, span, k, P, tw, rr, inv);
                 }
             }
         }
@@ -189,7 +201,7 @@ __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
         const double2 *src = in + rw * L;
         for (int j = threadIdx.x; j < L; j += blockDim.x) buf[perm[j]] = src[j];
         __syncthreads();
-        dft_passes(buf, 1, d, W, inv);
+        dft_passes(buf, 1, d, W, W + L, inv);
         double2 *dst = out + rw * L;
         for (int j = threadIdx.x; j < L; j += blockDim.x) dst[j] = buf[j];
         __syncthreads();
@@ -283,7 +295,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         }
     }
     __syncthreads();
-    dft_passes(buf, 2, d, Wt, true);
+    dft_passes(buf, 2, d, Wt, W + L, true);
     double2 *up = grid + (int64_t)(r_count + rr) * L;
     double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
     for (int j = threadIdx.x; j < L; j += blockDim.x) {
@@ -344,7 +356,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
             }
     }
     __syncthreads();
-    dft_passes(buf, 2, d, Wt, false);
+    dft_passes(buf, 2, d, Wt, W + L, false);
     const double w = weights[n + r];
     const double invL = 1.0 / (double)L;
     const int mtop = 2 * n - 1;
@@ -529,11 +541,16 @@ DftDesc make_desc(const bfsht_plan *pl) {
     d.L = (int)pl->dft_L;
     d.nrad = (int)pl->dft_radix.size();
     int64_t span = 1;
+    int tw = 0, ro = 0;
     for (int i = 0; i < d.nrad; ++i) {
         d.radix[i] = pl->dft_radix[i];
         // ceil(2^32 / span): exact for the quotients used (x < L <= 2^20,
         // verified exhaustively in bf_dft_prepare)
         d.span_inv[i] = span == 1 ? 0u : (unsigned)(((1ULL << 32) + span - 1) / span);
+        d.tw_off[i] = tw;
+        d.root_off[i] = ro;
+        tw += (int)((pl->dft_radix[i] - 1) * span);
+        ro += pl->dft_radix[i];
         span *= pl->dft_radix[i];
     }
     return d;
@@ -582,7 +599,7 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
             bfsht_set_error("DFT length has a prime factor above 128 (needs Bluestein)");
             return -4;
         }
-    std::vector<double> w(2 * L), tw(2 * L);
+    std::vector<double> w(2 * L), tw(2 * L), wt;
     std::vector<int32_t> perm(L);
     const double two_pi = 6.283185307179586476925286766559;
     for (int64_t k = 0; k < L; ++k) {
@@ -601,12 +618,36 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         tw[2 * b] = t.real();
         tw[2 * b + 1] = t.imag();
     }
+    // pass table: [0, L) inter-pass twiddles, pass after pass, entry
+    // (q-1)*span + k = w[q k L/(span P)]; then the radix roots of every
+    // pass, w[t L/P] for t < P (the same values the flat table held)
+    {
+        wt.assign(2 * L, 0.0);
+        int64_t span = 1, off = 0;
+        for (int p : rad) {
+            const int64_t tstep = L / (span * p);
+            for (int q = 1; q < p; ++q)
+                for (int64_t k = 0; k < span; ++k) {
+                    const int64_t e = (q * k * tstep) % L;
+                    wt[2 * (off + (q - 1) * span + k)] = w[2 * e];
+                    wt[2 * (off + (q - 1) * span + k) + 1] = w[2 * e + 1];
+                }
+            off += (p - 1) * span;
+            span *= p;
+        }
+        for (int p : rad)
+            for (int t = 0; t < p; ++t) {
+                const int64_t e = t * (L / p);
+                wt.push_back(w[2 * e]);
+                wt.push_back(w[2 * e + 1]);
+            }
+    }
     for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw})
         if (p) cudaFree(p);
-    BF_CUDA(cudaMalloc(&pl->dft_w, 16 * L));
+    BF_CUDA(cudaMalloc(&pl->dft_w, 8 * wt.size()));
     BF_CUDA(cudaMalloc(&pl->dft_tw, 16 * L));
     BF_CUDA(cudaMalloc(&pl->dft_perm, 4 * L));
-    BF_CUDA(cudaMemcpy(pl->dft_w, w.data(), 16 * L, cudaMemcpyHostToDevice));
+    BF_CUDA(cudaMemcpy(pl->dft_w, wt.data(), 8 * wt.size(), cudaMemcpyHostToDevice));
     BF_CUDA(cudaMemcpy(pl->dft_tw, tw.data(), 16 * L, cudaMemcpyHostToDevice));
     BF_CUDA(cudaMemcpy(pl->dft_perm, perm.data(), 4 * L, cudaMemcpyHostToDevice));
     pl->dft_radix = rad;

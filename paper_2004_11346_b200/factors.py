@@ -297,6 +297,32 @@ def cid(oracle, cfg, rng=None):
         f"{cap} (last ratio {last:.3e})", cap=cap, tail_ratio=last)
 
 
+def _pinv(a, rcond):
+    """np.linalg.pinv (LAPACK gesdd), as the reference calls it
+    (lowrank.py:370-372).  gesdd can fail to converge on strongly graded
+    blocks — the reference planner itself raises LinAlgError at N=4096,
+    tol 1e-10, m=5561 (checked by running it) — and only then is the same
+    pseudo-inverse formed from the QR-iteration driver gesvd: singular
+    values above rcond * max(s) inverted, the rest dropped (numpy's pinv
+    rule).  Factors of every order the reference can plan are unchanged."""
+    try:
+        return np.linalg.pinv(a, rcond=rcond)
+    except np.linalg.LinAlgError:
+        u, s, vt = scipy.linalg.svd(a, full_matrices=False, lapack_driver="gesvd")
+        keep = s > rcond * (s.max() if s.size else 0.0)
+        inv = np.zeros_like(s)
+        inv[keep] = 1.0 / s[keep]
+        return (vt.T * inv) @ u.T
+
+
+def _svd(a):
+    """np.linalg.svd (gesdd) with the same gesvd fallback as _pinv."""
+    try:
+        return np.linalg.svd(a)
+    except np.linalg.LinAlgError:
+        return scipy.linalg.svd(a, lapack_driver="gesvd")
+
+
 def rsvd(oracle, row_samples, col_samples, rank, oversample=2, rng=None):
     """Sampled rank-r SVD (Algorithm 1, lowrank.py:335-375)."""
     if rng is None:
@@ -323,10 +349,10 @@ def rsvd(oracle, row_samples, col_samples, rank, oversample=2, rng=None):
         m, size=min(row_samples.size, m), replace=False)])
     cols_aug = np.concatenate([pick_c, rng.choice(
         n, size=min(col_samples.size, n), replace=False)])
-    core = np.linalg.pinv(qc[rows_aug, :], rcond=1e-13) \
+    core = _pinv(qc[rows_aug, :], 1e-13) \
         @ oracle.block(rows_aug, cols_aug) \
-        @ np.linalg.pinv(qr_[cols_aug, :].T, rcond=1e-13)
-    u_m, s, vt_m = np.linalg.svd(core)
+        @ _pinv(qr_[cols_aug, :].T, 1e-13)
+    u_m, s, vt_m = _svd(core)
     return LowRankFactor(u=qc @ u_m[:, :r], s=s[:r], v=qr_ @ vt_m[:r, :].T)
 
 

@@ -25,7 +25,7 @@ payload streamed from HBM — what a GPU holding the whole plan would
 spend, up to per-stage tail effects of the smaller chunks.  Planning,
 packing and upload are host work and reported separately.
 """
-import os
+import sys
 import time
 
 import numpy as np
@@ -95,7 +95,7 @@ class ChunkedSht:
     chunk (default: ``plan_orders`` in ``processes`` host processes)."""
 
     def __init__(self, n, nchunks, params=None, tau=None, n0=None, processes=0,
-                 planner=None, reserve_bytes=24 << 30, device=None):
+                 planner=None, reserve_bytes=24 << 30, device=None, verbose=False):
         import torch
         from .api import DevicePlan
         from .legendre import gauss_legendre
@@ -113,6 +113,7 @@ class ChunkedSht:
                                    processes=processes, quadrature=self.quadrature)
         self.planner = planner
         self.reserve_bytes = int(reserve_bytes)
+        self.verbose = verbose
         self.chunks, self.layout, self.block, entries = chunk_layout(n, self.nchunks)
         dev = self.device
         self.ybuf = torch.zeros((entries, NRHS), dtype=torch.float64, device=dev)
@@ -232,6 +233,14 @@ class ChunkedSht:
                                   "pack_upload_s": tu, "resident": False})
             torch.cuda.synchronize()
             rep["chunks"][-1]["resident"] = self._keep(c, dp)
+            rep["chunks"][-1]["tile_gb"] = dp.packed.tile_bytes / 1e9
+            if self.verbose:
+                free, total = torch.cuda.mem_get_info(self.device)
+                print(f"[ooc] fwd chunk {c}: {len(orders)} orders, tiles "
+                      f"{dp.packed.tile_bytes / 1e9:.1f} GB, arena "
+                      f"{dp.arena.numel() * 8 / 1e9:.2f} GB, plan {tp:.1f} s, pack+upload "
+                      f"{tu:.1f} s, resident {rep['chunks'][-1]['resident']}, device used "
+                      f"{(total - free) / 1e9:.1f} GB", file=sys.stderr, flush=True)
             del dp, coeffs
             torch.cuda.empty_cache()
         st = self._stream()

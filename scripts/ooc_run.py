@@ -52,7 +52,7 @@ def main():
     params = SamplingConfig(tolerance=args.tol)
     t0 = time.perf_counter()
     run = ChunkedSht(n, args.chunks, params=params, processes=args.procs,
-                     reserve_bytes=int(args.reserve_gb * (1 << 30)))
+                     reserve_bytes=int(args.reserve_gb * (1 << 30)), verbose=True)
     flat = synthetic_coeffs(n, seed=3)
     grid = torch.empty((2 * n, L), dtype=torch.complex128, device="cuda")
     fwd = run.forward(flat, grid)

@@ -79,3 +79,24 @@ def test_threaded_plan_matches_serial():
     a = plan_alt(128, 128, n0=32, workers=1)
     b = plan_alt(128, 128, n0=32, workers=4)
     assert plan_digest(a) == plan_digest(b)
+
+
+def test_gesdd_nonconvergence_fallback_n4096():
+    # The reference planner raises LinAlgError ("SVD did not converge",
+    # LAPACK gesdd inside np.linalg.pinv, lowrank.py:370-372) at N=4096,
+    # tol 1e-10, m=5561 — checked by running it.  Here the pseudo-inverse
+    # falls back to gesvd for that block only; the plan must still meet
+    # its tolerance against the dense ALT.
+    import oracle.apply as OA
+    import oracle.dense as OD
+    from threadpoolctl import threadpool_limits
+    from paper_2004_11346_b200 import SamplingConfig, gauss_legendre, plan_alt
+    n, m = 4096, 5561
+    q = gauss_legendre(2 * n)
+    with threadpool_limits(limits=1):
+        p = plan_alt(n, m, SamplingConfig(tolerance=1e-10), quadrature=q)
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(2 * n - m) + 1j * rng.standard_normal(2 * n - m)
+    got = OA.alt_forward(p, v)
+    want = OD.dense_alt_forward(n, m, v, q)
+    assert np.linalg.norm(got - want) <= 1e-9 * np.linalg.norm(want)
