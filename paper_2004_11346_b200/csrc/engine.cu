@@ -278,8 +278,18 @@ __device__ __forceinline__ uint32_t tile_dst(const bf_op &op) {
 
 // value p * 2^e flushed to 0 below mag_min, exactly ldexp(p, e) then the
 // flush (recur.c emit): a normal p with a normal result only shifts its
-// exponent field; results below 2^-1022 are under mag_min (~2^-1010) anyway
-__device__ __forceinline__ double emit_value(double p, int e, double mag_min) {
+// exponent field; results below 2^-1022 are under mag_min (~2^-1010) anyway.
+// The flush compares magnitudes as IEEE bit patterns (integer pipe), which
+// orders finite values exactly like the floating-point compare.
+// |v| as its IEEE bit pattern, built from the two 32-bit halves so that the
+// compiler keeps it on the integer pipe (a 64-bit mask becomes a DADD |v|)
+__device__ __forceinline__ long long abits(double v) {
+    const unsigned hi = (unsigned)__double2hiint(v) & 0x7fffffffu;
+    const unsigned lo = (unsigned)__double2loint(v);
+    return (long long)(((unsigned long long)hi << 32) | lo);
+}
+
+__device__ __forceinline__ double emit_value(double p, int e, long long mag_bits) {
     const long long b = __double_as_longlong(p);
     const int ef = (int)((b >> 52) & 0x7ff);
     const int ne = ef + e;
@@ -290,20 +300,57 @@ __device__ __forceinline__ double emit_value(double p, int e, double mag_min) {
         v = 0.0;
     else
         v = ldexp(p, e);   // zero / subnormal p, or overflow: rare
-    return fabs(v) < mag_min ? 0.0 : v;
+    return abits(v) < mag_bits ? 0.0 : v;
+}
+
+// One recurrence step without the range test (recur.h bfr_step's
+// arithmetic: three roundings, one subtraction, no FMA).
+__device__ __forceinline__ void rec_step(double x, double a, double b, double &pp, double &pc) {
+    const double t1 = __dmul_rn(x, pc);
+    const double t2 = __dmul_rn(a, t1);
+    const double t3 = __dmul_rn(b, pp);
+    const double pn = __dsub_rn(t2, t3);
+    pp = pc;
+    pc = pn;
+}
+
+// bfr_step's range test and exact 2^-+1000 rescale, on IEEE bit patterns:
+// |p| > 2^500 <=> abits(p) > 0x5F3..., |p| < 2^-500 <=> abits(p) < 0x20B...
+__device__ __forceinline__ void rec_rescale(double &pp, double &pc, int &e) {
+    const long long ua = abits(pc), ub = abits(pp);
+    const long long mx = ua > ub ? ua : ub;
+    if (mx > 0x5F30000000000000LL) {
+        pc = __dmul_rn(pc, 0x1p-1000);
+        pp = __dmul_rn(pp, 0x1p-1000);
+        e += 1000;
+    } else if (mx < 0x20B0000000000000LL && mx > 0) {
+        pc = __dmul_rn(pc, 0x1p1000);
+        pp = __dmul_rn(pp, 0x1p1000);
+        e -= 1000;
+    }
 }
 
 // Regenerate a dense turning tile in place from its seed block:
-// lane r re-runs row r's degree recurrence exactly as the planner did
-// (recur.h; pkg/src/bfsht/kernels/_recur_cy.pyx:45-66), two steps per
-// column (degrees of one parity), emitting ldexp(p, e) flushed below
-// MAG_MIN — the stored values bit for bit (tests/test_regen_pack.py,
-// tests/test_gpu_regen.py).  The tile's step coefficients arrive in one
-// coalesced load (lane c holds column c's two steps) and are broadcast by
-// shuffles; four columns are emitted per 32-byte shared store.  Padding
-// rows / columns are written as zeros.
+// lane r re-runs row r's degree recurrence as the planner did (recur.h;
+// pkg/src/bfsht/kernels/_recur_cy.pyx:45-66), two steps per column
+// (degrees of one parity), emitting ldexp(p, e) flushed below MAG_MIN —
+// the stored values bit for bit (tests/test_regen_pack.py,
+// tests/test_gpu_regen.py).
+//
+// Cost shape: the reference tests the (mantissa, 2^e) range after every
+// step; here it is tested once per column, after both steps.  The rescale
+// multiplies by an exact power of two, and a step grows |p| by at most
+// alpha |x| + beta < 2^7, so within two steps the mantissas stay far inside
+// the normal range (below 2^514; a nonzero difference of two rounded
+// products near 2^-500 is above 2^-560), every intermediate is the
+// reference's value times 2^(1000 j), and
+// every emitted ldexp(p, e) is the same number; the test itself runs on
+// the integer pipe.  The step coefficients (alpha, beta of the column's
+// two steps) are one warp-uniform 32-byte load per column from the L1-
+// resident table, issued a column ahead, instead of four shuffles.
+// Padding rows / columns are written as zeros.
 __device__ __noinline__ void regen_tile(const double *__restrict__ rec,
-                                        const double *__restrict__ xpos, double mag_min, int R,
+                                        const double *__restrict__ xpos, long long mag_bits, int R,
                                         int C, double *T, int lane) {
     const int C4 = (C + 3) >> 2, R4 = (R + 3) >> 2;
     const double *sb = T + kTileDoubles - bf_seed_doubles(R);
@@ -317,11 +364,11 @@ __device__ __noinline__ void regen_tile(const double *__restrict__ rec,
         e = (int)sb[4 + 3 * lane];
         x = __ldg(xpos + r_a + lane);
     }
-    double2 s0 = make_double2(0.0, 0.0), s1 = s0;
-    if (lane + 1 < C) {
-        const double2 *ab = reinterpret_cast<const double2 *>(rec + rb) + 2 * lane;
-        s0 = __ldg(ab);
-        s1 = __ldg(ab + 1);
+    const double2 *ab = reinterpret_cast<const double2 *>(rec + rb);
+    double2 n0 = make_double2(0.0, 0.0), n1 = n0;
+    if (C > 1) {
+        n0 = __ldg(ab);
+        n1 = __ldg(ab + 1);
     }
     __syncwarp();
     const bool live = lane < R;
@@ -331,15 +378,17 @@ __device__ __noinline__ void regen_tile(const double *__restrict__ rec,
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int c = 4 * cb + i;
-            v[i] = (live && c < C) ? emit_value(pc, e, mag_min) : 0.0;
+            v[i] = (live && c < C) ? emit_value(pc, e, mag_bits) : 0.0;
             if (c + 1 < C) {
-                const double a0 = __shfl_sync(0xffffffffu, s0.x, c);
-                const double b0 = __shfl_sync(0xffffffffu, s0.y, c);
-                const double a1 = __shfl_sync(0xffffffffu, s1.x, c);
-                const double b1 = __shfl_sync(0xffffffffu, s1.y, c);
+                const double2 s0 = n0, s1 = n1;
+                if (c + 2 < C) {
+                    n0 = __ldg(ab + 2 * (c + 1));
+                    n1 = __ldg(ab + 2 * (c + 1) + 1);
+                }
                 if (live) {
-                    bfr_step(x, a0, b0, &pp, &pc, &e);
-                    bfr_step(x, a1, b1, &pp, &pc, &e);
+                    rec_step(x, s0.x, s0.y, pp, pc);
+                    rec_step(x, s1.x, s1.y, pp, pc);
+                    rec_rescale(pp, pc, e);
                 }
             }
         }
@@ -611,7 +660,7 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
             }
         } else {
             if (op.flags & BF_OPF_REGEN)
-                regen_tile(a.rec, a.xpos, a.mag_min, op.R, op.C, ring.tile[s], lane);
+                regen_tile(a.rec, a.xpos, __double_as_longlong(a.mag_min), op.R, op.C, ring.tile[s], lane);
             double e[G][4][2];
             tile_product<NR>(op, ring.tile[s], V, ring.zero, lane, e);
             const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;

@@ -236,61 +236,79 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     const int mtop = 2 * n - 1;
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
-    // bins in batches of kBatch per thread: every load of a batch is issued
-    // before any is used (the layout lookup and the node-half loads are
-    // otherwise a chain of dependent DRAM latencies per bin)
-    constexpr int kBatch = 8;
-    for (int b0 = threadIdx.x; b0 < L; b0 += kBatch * blockDim.x) {
-        double2 go[kBatch], ge[kBatch], t[kBatch];
-        int p[kBatch];
+    // one thread per order |m|: its odd and even node-half entries (+m and
+    // -m, 32 B each, adjacent in Yr) are read whole and feed the two bins
+    // m and L-m of both rows, so every loaded sector is fully used; orders
+    // in batches of kBatch per thread, every load of a batch issued before
+    // any is used (otherwise a chain of dependent DRAM latencies)
+    constexpr int kBatch = 4;
+    const int nord = mtop + 1;
+    for (int a0 = threadIdx.x; a0 < nord; a0 += kBatch * blockDim.x) {
+        double2 op[kBatch], on[kBatch], ep[kBatch], en[kBatch], tp[kBatch], tn[kBatch];
+        int pp[kBatch], pn[kBatch];
         if (ystride > 0) {
             const double *rowp = arena + (yr + (int64_t)rr * ystride) * ew;
 #pragma unroll
             for (int i = 0; i < kBatch; ++i) {
-                const int b = b0 + i * blockDim.x;
-                const bool ok = b < L;
-                const int m = ok ? (b <= mtop ? b : b - L) : 0;
-                const int am = m < 0 ? -m : m;
-                const int sel = (ok && b > mtop) ? 2 : 0;
-                go[i] = ge[i] = make_double2(0.0, 0.0);
+                const int am = a0 + i * blockDim.x;
+                const bool ok = am < nord;
+                op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
                 if (ok) {
-                    go[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am) * ew + sel);
-                    ge[i] = *reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew + sel);
+                    const double2 *eo = reinterpret_cast<const double2 *>(rowp + (2 * am) * ew);
+                    const double2 *ee = reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew);
+                    op[i] = eo[0];
+                    on[i] = eo[1];
+                    ep[i] = ee[0];
+                    en[i] = ee[1];
                 }
-                t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
-                p[i] = ok ? perm[b] : 0;
+                const int bn = am > 0 ? L - am : 0;
+                tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
+                tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+                pp[i] = ok ? perm[am] : 0;
+                pn[i] = ok ? perm[bn] : 0;
             }
         } else {
         bf_half ho[kBatch], he[kBatch];
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
-            const int b = b0 + i * blockDim.x;
-            const int m = b < L ? (b <= mtop ? b : b - L) : 0;
-            const int am = m < 0 ? -m : m;
+            const int am = a0 + i * blockDim.x < nord ? a0 + i * blockDim.x : 0;
             ho[i] = halves[2 * am];
             he[i] = halves[2 * am + 1];
         }
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
-            const int b = b0 + i * blockDim.x;
-            const bool ok = b < L;
-            const int sel = (ok && b > mtop) ? 2 : 0;
-            go[i] = ge[i] = make_double2(0.0, 0.0);
-            if (ok && ho[i].ncols > 0)
-                go[i] = *reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew + sel);
-            if (ok && he[i].ncols > 0)
-                ge[i] = *reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew + sel);
-            t[i] = ok ? tw[b] : make_double2(0.0, 0.0);
-            p[i] = ok ? perm[b] : 0;
+            const int am = a0 + i * blockDim.x;
+            const bool ok = am < nord;
+            op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
+            if (ok && ho[i].ncols > 0) {
+                const double2 *eo = reinterpret_cast<const double2 *>(
+                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew);
+                op[i] = eo[0];
+                on[i] = eo[1];
+            }
+            if (ok && he[i].ncols > 0) {
+                const double2 *ee = reinterpret_cast<const double2 *>(
+                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew);
+                ep[i] = ee[0];
+                en[i] = ee[1];
+            }
+            const int bn = am > 0 && ok ? L - am : 0;
+            tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
+            tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+            pp[i] = ok ? perm[am] : 0;
+            pn[i] = ok ? perm[bn] : 0;
         }
         }
 #pragma unroll
         for (int i = 0; i < kBatch; ++i) {
-            if (b0 + i * blockDim.x < L) {
-                buf[p[i]] = cmul(make_double2(ge[i].x + go[i].x, ge[i].y + go[i].y), t[i]);
-                buf[L + p[i]] = cmul(make_double2(ge[i].x - go[i].x, ge[i].y - go[i].y), t[i]);
+            const int am = a0 + i * blockDim.x;
+            if (am < nord) {
+                buf[pp[i]] = cmul(make_double2(ep[i].x + op[i].x, ep[i].y + op[i].y), tp[i]);
+                buf[L + pp[i]] = cmul(make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y), tp[i]);
+                if (am > 0) {
+                    buf[pn[i]] = cmul(make_double2(en[i].x + on[i].x, en[i].y + on[i].y), tn[i]);
+                    buf[L + pn[i]] = cmul(make_double2(en[i].x - on[i].x, en[i].y - on[i].y), tn[i]);
+                }
             }
         }
     }
@@ -360,14 +378,18 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double w = weights[n + r];
     const double invL = 1.0 / (double)L;
     const int mtop = 2 * n - 1;
-    for (int b0 = threadIdx.x; b0 < L; b0 += kBatch * blockDim.x) {
-        bf_half ho[kBatch], he[kBatch];
-        double2 t[kBatch];
+    // one thread per order |m|: bins m and L-m of both rows give the +m and
+    // -m halves of its odd and even node-half entries, each written whole
+    // (32 B, full sectors) rather than as two 16-B halves at different times
+    const int nord = mtop + 1;
+    constexpr int kOut = 4;
+    for (int a0 = threadIdx.x; a0 < nord; a0 += kOut * blockDim.x) {
+        bf_half ho[kOut], he[kOut];
+        double2 tp[kOut], tn[kOut];
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int b = b0 + i * blockDim.x;
-            const int m = b < L ? (b <= mtop ? b : b - L) : 0;
-            const int am = m < 0 ? -m : m;
+        for (int i = 0; i < kOut; ++i) {
+            const int am0 = a0 + i * blockDim.x;
+            const int am = am0 < nord ? am0 : 0;
             if (ys) {
                 const int yo = ys[2 * am], ye = ys[2 * am + 1];
                 ho[i].y = yo;
@@ -380,29 +402,39 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
                 ho[i] = halves[2 * am];
                 he[i] = halves[2 * am + 1];
             }
-            t[i] = b < L ? tw[b] : make_double2(0.0, 0.0);
+            tp[i] = tw[am];
+            tn[i] = tw[am > 0 ? L - am : 0];
         }
 #pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int b = b0 + i * blockDim.x;
-            if (b >= L) continue;
-            const int m = b <= mtop ? b : b - L;
-            const int sel = m < 0 ? 2 : 0;
-            const double2 tc = make_double2(t[i].x, -t[i].y);
-            double2 sa = buf[b], sb = buf[L + b];
-            sa = cmul(make_double2(sa.x * invL, sa.y * invL), tc);
-            sb = cmul(make_double2(sb.x * invL, sb.y * invL), tc);
+        for (int i = 0; i < kOut; ++i) {
+            const int am = a0 + i * blockDim.x;
+            if (am >= nord) continue;
+            const int bn = L - am;
+            double2 sa = buf[am], sb = buf[L + am];
+            const double2 cp = make_double2(tp[i].x, -tp[i].y);
+            sa = cmul(make_double2(sa.x * invL, sa.y * invL), cp);
+            sb = cmul(make_double2(sb.x * invL, sb.y * invL), cp);
+            double2 na = make_double2(0.0, 0.0), nb = na;
+            if (am > 0) {
+                const double2 cn = make_double2(tn[i].x, -tn[i].y);
+                na = buf[bn];
+                nb = buf[L + bn];
+                na = cmul(make_double2(na.x * invL, na.y * invL), cn);
+                nb = cmul(make_double2(nb.x * invL, nb.y * invL), cn);
+            }
             if (ho[i].ncols > 0) {
-                double *e = arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew;
-                *reinterpret_cast<double2 *>(e + sel) =
-                    make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
-                if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+                double2 *e = reinterpret_cast<double2 *>(
+                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew);
+                e[0] = make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
+                e[1] = am > 0 ? make_double2(w * (na.x - nb.x), w * (na.y - nb.y))
+                              : make_double2(0.0, 0.0);
             }
             if (he[i].ncols > 0) {
-                double *e = arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew;
-                *reinterpret_cast<double2 *>(e + sel) =
-                    make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
-                if (m == 0) *reinterpret_cast<double2 *>(e + 2) = make_double2(0.0, 0.0);
+                double2 *e = reinterpret_cast<double2 *>(
+                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew);
+                e[0] = make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
+                e[1] = am > 0 ? make_double2(w * (na.x + nb.x), w * (na.y + nb.y))
+                              : make_double2(0.0, 0.0);
             }
         }
     }

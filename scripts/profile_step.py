@@ -18,10 +18,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--tol", type=float, default=1e-12)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--regen", type=float, default=0.0)
 a = ap.parse_args()
 n = a.n
 plans = plan_orders(n, range(2 * n), SamplingConfig(tolerance=a.tol), processes=0)
-dp = DevicePlan(plans)
+dp = DevicePlan(plans, regen=a.regen)
 print("stages fwd/inv", dp.stats["stages_fwd"], dp.stats["stages_inv"], flush=True)
 c = torch.from_numpy(synthetic_coeffs(n)).cuda()
 g = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128, device="cuda")
