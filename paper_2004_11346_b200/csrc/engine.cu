@@ -265,22 +265,29 @@ __device__ __forceinline__ int gather_src(const StageArgs &a, const Rec &r, int 
 }
 
 __device__ __forceinline__ uint32_t tile_bytes(const bf_op &op) {
-    return (op.flags & BF_OPF_REGEN) ? (uint32_t)bf_seed_doubles(op.R) * 8u
+    return (op.flags & BF_OPF_REGEN) ? (uint32_t)bf_seed_doubles(op.R, op.C) * 8u
                                      : (uint32_t)bf_tile_doubles(op.R, op.C) * 8u;
 }
 
-// Where a tile's bytes land in its ring slot: values at the start; a seed
-// block at the end, so the regenerated values can be written from the
-// start once every lane holds its row's seed.
-__device__ __forceinline__ uint32_t tile_dst(const bf_op &op) {
-    return (op.flags & BF_OPF_REGEN) ? (uint32_t)(kTileDoubles - bf_seed_doubles(op.R)) : 0u;
+// Where a tile's bytes land in its ring slot: at the start, stored values
+// and regeneration seed blocks alike (the seeds are read into registers
+// before any value is written).  A regenerated tile's step coefficients are
+// staged separately (regen_coef).
+__device__ __forceinline__ uint32_t tile_dst(const bf_op &) { return 0u; }
+
+// Ring-slot position (doubles) of column c's four step coefficients
+// (alpha, beta of its two steps) for a regenerated tile with C4 column
+// blocks, chosen so that no value is written there before the coefficient
+// has been read and no seed is staged there: with <= 7 column blocks the
+// free tail of the slot (values end below 7 x 8 x 16 = 896 doubles); with 8,
+// column blocks 3 and 7 of row blocks 2-7 — the blocks the two chains write
+// last (seeds occupy row blocks 0-1).
+__device__ __forceinline__ int regen_coef(int c, int C4) {
+    if (C4 < BF_T / 4) return 896 + 4 * c;
+    const int k = c >> 2;
+    return (2 + (k >> 1)) * 128 + ((k & 1) ? 7 : 3) * 16 + 4 * (c & 3);
 }
 
-// value p * 2^e flushed to 0 below mag_min, exactly ldexp(p, e) then the
-// flush (recur.c emit): a normal p with a normal result only shifts its
-// exponent field; results below 2^-1022 are under mag_min (~2^-1010) anyway.
-// The flush compares magnitudes as IEEE bit patterns (integer pipe), which
-// orders finite values exactly like the floating-point compare.
 // |v| as its IEEE bit pattern, built from the two 32-bit halves so that the
 // compiler keeps it on the integer pipe (a 64-bit mask becomes a DADD |v|)
 __device__ __forceinline__ long long abits(double v) {
@@ -289,18 +296,19 @@ __device__ __forceinline__ long long abits(double v) {
     return (long long)(((unsigned long long)hi << 32) | lo);
 }
 
+// ldexp(p, e) flushed to 0 below mag_min (recur.c emit), branch-free on the
+// integer pipe: a normal p with a normal result only shifts its exponent
+// field (exact); a result below 2^-1022 is under mag_min (~2^-1010) and
+// flushes anyway; p = 0 gives 0.  (p is never subnormal or huge here: the
+// mantissas stay within [2^-560, 2^560] or are exactly 0, see regen_tile.)
+// The flush compares magnitudes as IEEE bit patterns, which orders finite
+// values exactly like the floating-point compare.
 __device__ __forceinline__ double emit_value(double p, int e, long long mag_bits) {
     const long long b = __double_as_longlong(p);
-    const int ef = (int)((b >> 52) & 0x7ff);
-    const int ne = ef + e;
-    double v;
-    if (ef != 0 && ne >= 1 && ne <= 2046)
-        v = __longlong_as_double(b + ((long long)e << 52));
-    else if (ef != 0 && ne < 1)
-        v = 0.0;
-    else
-        v = ldexp(p, e);   // zero / subnormal p, or overflow: rare
-    return abits(v) < mag_bits ? 0.0 : v;
+    const int ef = (int)(((unsigned)__double2hiint(p) >> 20) & 0x7ffu);
+    const long long v = (ef != 0 && ef + e >= 1) ? b + ((long long)e << 52) : 0LL;
+    const double d = __longlong_as_double(v);
+    return abits(d) < mag_bits ? 0.0 : d;
 }
 
 // One recurrence step without the range test (recur.h bfr_step's
@@ -314,20 +322,18 @@ __device__ __forceinline__ void rec_step(double x, double a, double b, double &p
     pc = pn;
 }
 
-// bfr_step's range test and exact 2^-+1000 rescale, on IEEE bit patterns:
-// |p| > 2^500 <=> abits(p) > 0x5F3..., |p| < 2^-500 <=> abits(p) < 0x20B...
+// bfr_step's range test and exact 2^-+1000 rescale, on IEEE bit patterns
+// (|p| > 2^500 <=> abits(p) > 0x5F3..., |p| < 2^-500 <=> abits(p) < 0x20B...),
+// branch-free: the scale factor is 1.0 (exact, no change) when in range.
 __device__ __forceinline__ void rec_rescale(double &pp, double &pc, int &e) {
     const long long ua = abits(pc), ub = abits(pp);
     const long long mx = ua > ub ? ua : ub;
-    if (mx > 0x5F30000000000000LL) {
-        pc = __dmul_rn(pc, 0x1p-1000);
-        pp = __dmul_rn(pp, 0x1p-1000);
-        e += 1000;
-    } else if (mx < 0x20B0000000000000LL && mx > 0) {
-        pc = __dmul_rn(pc, 0x1p1000);
-        pp = __dmul_rn(pp, 0x1p1000);
-        e -= 1000;
-    }
+    const bool big = mx > 0x5F30000000000000LL;
+    const bool small = mx < 0x20B0000000000000LL && mx > 0;
+    const double f = big ? 0x1p-1000 : (small ? 0x1p1000 : 1.0);
+    pc = __dmul_rn(pc, f);
+    pp = __dmul_rn(pp, f);
+    e += big ? 1000 : (small ? -1000 : 0);
 }
 
 // Regenerate a dense turning tile in place from its seed block:
@@ -337,68 +343,126 @@ __device__ __forceinline__ void rec_rescale(double &pp, double &pc, int &e) {
 // the stored values bit for bit (tests/test_regen_pack.py,
 // tests/test_gpu_regen.py).
 //
-// Cost shape: the reference tests the (mantissa, 2^e) range after every
-// step; here it is tested once per column, after both steps.  The rescale
-// multiplies by an exact power of two, and a step grows |p| by at most
-// alpha |x| + beta < 2^7, so within two steps the mantissas stay far inside
-// the normal range (below 2^514; a nonzero difference of two rounded
-// products near 2^-500 is above 2^-560), every intermediate is the
-// reference's value times 2^(1000 j), and
-// every emitted ldexp(p, e) is the same number; the test itself runs on
-// the integer pipe.  The step coefficients (alpha, beta of the column's
-// two steps) are one warp-uniform 32-byte load per column from the L1-
-// resident table, issued a column ahead, instead of four shuffles.
-// Padding rows / columns are written as zeros.
-__device__ __noinline__ void regen_tile(const double *__restrict__ rec,
-                                        const double *__restrict__ xpos, long long mag_bits, int R,
-                                        int C, double *T, int lane) {
-    const int C4 = (C + 3) >> 2, R4 = (R + 3) >> 2;
-    const double *sb = T + kTileDoubles - bf_seed_doubles(R);
-    const int r_a = __double2loint(sb[0]);
-    const long long rb = __double_as_longlong(sb[1]);
-    double pp = 0.0, pc = 0.0, x = 0.0;
-    int e = 0;
-    if (lane < R) {
-        pp = sb[2 + 3 * lane];
-        pc = sb[3 + 3 * lane];
-        e = (int)sb[4 + 3 * lane];
-        x = __ldg(xpos + r_a + lane);
-    }
-    const double2 *ab = reinterpret_cast<const double2 *>(rec + rb);
-    double2 n0 = make_double2(0.0, 0.0), n1 = n0;
-    if (C > 1) {
-        n0 = __ldg(ab);
-        n1 = __ldg(ab + 1);
-    }
-    __syncwarp();
-    const bool live = lane < R;
-    double *row = T + (lane >> 2) * C4 * 16 + (lane & 3) * 4;
-    for (int cb = 0; cb < C4; ++cb) {
-        double v[4];
+// Cost shape (measured: the first version spent ~2500 warp instructions
+// per tile, latency-bound on branches and per-step range tests): the
+// reference tests the (mantissa, 2^e) range after every step; here it is
+// tested once per 4 columns (8 steps), branch-free.  The rescale multiplies
+// by an exact power of two; a step grows |p| by at most alpha |x| + beta
+// < 2^7 and shrinks the larger of |p_k|, |p_k-1| by at most ~2, so between
+// tests the mantissas stay inside [2^-510, 2^556] (a nonzero difference of
+// two rounded products there is above 2^-560): every intermediate is the
+// reference's value times 2^(1000 j), and every emitted ldexp(p, e) is the
+// same number.  Step coefficients (alpha, beta of the column's two steps)
+// are a warp-uniform 32-byte load per column, issued a column ahead.
+// Padding rows / columns come out as zeros (padding lanes run x = p = 0).
+// One block step of K chains (chain h covers columns [16h, ...)): emit
+// column block j of each chain, advance each by its 4 columns, range-test.
+// Emission with e fixed for the block, as one 64-bit compare: for a value
+// that survives the flush (|p| 2^e >= mag_min, hence normal), its bits are
+// abits(p) + (e << 52), so "keep" is abits(p) >= mag_bits - (e << 52); a
+// kept value is that exponent shift of p (exact).  e <= -1700 can only give
+// flushed values (|p| < 2^560).  p = 0 is never kept.
+template <int K>
+__device__ __forceinline__ void regen_block(const double *T, int C, int C4, int j, double x,
+                                            double (&pp)[K], double (&pc)[K], int (&e)[K],
+                                            long long mag_bits, double (&v)[K][4]) {
+    const int cend0 = C < BF_SEED_SPLIT ? C : BF_SEED_SPLIT;
+#pragma unroll
+    for (int h = 0; h < K; ++h) {
+        // this block's coefficients, 4 columns x (alpha, beta) x 2 steps,
+        // contiguous in the slot (regen_coef), loaded before the chain work
+        double2 cf[8];
+        const double2 *base =
+            reinterpret_cast<const double2 *>(T + regen_coef(h * BF_SEED_SPLIT + 4 * j, C4));
+#pragma unroll
+        for (int t = 0; t < 8; ++t) cf[t] = base[t];
+        const long long e52 = (long long)e[h] << 52;
+        const long long thr = e[h] <= -1700 ? 0x7fffffffffffffffLL : mag_bits - e52;
+        const int cend = h == 0 ? cend0 : C;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int c = 4 * cb + i;
-            v[i] = (live && c < C) ? emit_value(pc, e, mag_bits) : 0.0;
-            if (c + 1 < C) {
-                const double2 s0 = n0, s1 = n1;
-                if (c + 2 < C) {
-                    n0 = __ldg(ab + 2 * (c + 1));
-                    n1 = __ldg(ab + 2 * (c + 1) + 1);
-                }
-                if (live) {
-                    rec_step(x, s0.x, s0.y, pp, pc);
-                    rec_step(x, s1.x, s1.y, pp, pc);
-                    rec_rescale(pp, pc, e);
+            const int c = h * BF_SEED_SPLIT + 4 * j + i;
+            const long long b = __double_as_longlong(pc[h]);
+            v[h][i] = (c < cend && abits(pc[h]) >= thr) ? __longlong_as_double(b + e52) : 0.0;
+            if (c + 1 < cend) {
+                rec_step(x, cf[2 * i].x, cf[2 * i].y, pp[h], pc[h]);
+                rec_step(x, cf[2 * i + 1].x, cf[2 * i + 1].y, pp[h], pc[h]);
+            }
+        }
+        rec_rescale(pp[h], pc[h], e[h]);
+    }
+}
+
+template <int K>
+__device__ __forceinline__ void regen_chains(const double *sb, const double *__restrict__ xpos,
+                                             long long mag_bits, int R, int C, double *T,
+                                             int lane) {
+    const int C4 = (C + 3) >> 2, R4 = (R + 3) >> 2;
+    const int r_a = __double2loint(sb[0]);
+    double pp[K], pc[K], x = 0.0;
+    int e[K];
+#pragma unroll
+    for (int h = 0; h < K; ++h) {
+        pp[h] = pc[h] = 0.0;
+        e[h] = 0;
+        if (lane < R) {
+            pp[h] = sb[2 + 3 * (h * R + lane)];
+            pc[h] = sb[3 + 3 * (h * R + lane)];
+            e[h] = (int)sb[4 + 3 * (h * R + lane)];
+        }
+    }
+    if (lane < R) x = __ldg(xpos + r_a + lane);
+    __syncwarp();   // seeds read: their slot region may now be overwritten
+    double *row = T + (lane >> 2) * C4 * 16 + (lane & 3) * 4;
+    const int nj = K == 1 ? C4 : BF_SEED_SPLIT / 4;
+#pragma unroll 1
+    for (int j = 0; j < nj; ++j) {
+        double v[K][4];
+        regen_block<K>(T, C, C4, j, x, pp, pc, e, mag_bits, v);
+        __syncwarp();   // every lane has read this block's coefficients
+        if (lane < R4 * 4) {
+#pragma unroll
+            for (int h = 0; h < K; ++h) {
+                const int cb = h * (BF_SEED_SPLIT / 4) + j;
+                if (cb < C4) {
+                    double2 *d = reinterpret_cast<double2 *>(row + cb * 16);
+                    d[0] = make_double2(v[h][0], v[h][1]);
+                    d[1] = make_double2(v[h][2], v[h][3]);
                 }
             }
         }
-        if (lane < R4 * 4) {
-            double2 *d = reinterpret_cast<double2 *>(row + cb * 16);
-            d[0] = make_double2(v[0], v[1]);
-            d[1] = make_double2(v[2], v[3]);
-        }
     }
     __syncwarp();
+}
+
+// Regenerate a dense turning tile in place from its seed block:
+// lane r re-runs row r's degree recurrence as the planner did (recur.h;
+// pkg/src/bfsht/kernels/_recur_cy.pyx:45-66), two steps per column
+// (degrees of one parity), emitting ldexp(p, e) flushed below MAG_MIN —
+// the stored values bit for bit (tests/test_regen_pack.py,
+// tests/test_gpu_regen.py).
+//
+// Cost shape.  The step is a chain of three dependent fp64 operations, so
+// one recurrence per lane is latency-bound (measured ~2500 warp
+// instructions and ~15 k cycles per tile in the first version): tiles
+// wider than 16 columns carry a second seed (the state at column 16), and
+// every lane runs the two column halves as two independent chains.  The
+// reference tests the (mantissa, 2^e) range after every step; here it is
+// tested once per 4 columns (8 steps), branch-free.  The rescale multiplies
+// by an exact power of two; a step grows |p| by at most alpha |x| + beta
+// < 2^7 and shrinks the larger of |p_k|, |p_k-1| by at most ~2, so between
+// tests the mantissas stay inside [2^-510, 2^556] (a nonzero difference of
+// two rounded products there is above 2^-560): every intermediate is the
+// reference's value times 2^(1000 j), and every emitted ldexp(p, e) is the
+// same number.  The step coefficients were staged into the slot at issue
+// time (cp.async, regen_coef) and are read as warp-uniform shared loads.
+// Padding rows / columns come out as zeros.
+__device__ __noinline__ void regen_tile(const double *__restrict__ xpos, long long mag_bits, int R,
+                                        int C, double *T, int lane) {
+    if (bf_seed_chains(C) == 2)
+        regen_chains<2>(T, xpos, mag_bits, R, C, T, lane);
+    else
+        regen_chains<1>(T, xpos, mag_bits, R, C, T, lane);
 }
 
 // Issue the loads of one op into ring slot s (whole warp).
@@ -438,6 +502,13 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing<NR> &ring, in
     }
     if ((op.flags & BF_OPF_LANEMAP) && lane < BF_SLOTS / 16)
         cp_async16(&ring.map[s][lane * 16], a.maps + (int64_t)op.aux * BF_SLOTS + lane * 16);
+    if ((op.flags & BF_OPF_REGEN) && lane + 1 < op.C) {
+        // lane c: column c's 4 step coefficients (32 B) from the rec table
+        double *d = ring.tile[s] + regen_coef(lane, (op.C + 3) >> 2);
+        const double *g = a.rec + (int64_t)op.aux + 4 * lane;
+        cp_async16(d, g);
+        cp_async16(d + 2, g + 2);
+    }
     cp_async_arrive(&ring.full[s]);
     if (lane == 0) {
         fence_proxy_async();
@@ -660,7 +731,7 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
             }
         } else {
             if (op.flags & BF_OPF_REGEN)
-                regen_tile(a.rec, a.xpos, __double_as_longlong(a.mag_min), op.R, op.C, ring.tile[s], lane);
+                regen_tile(a.xpos, __double_as_longlong(a.mag_min), op.R, op.C, ring.tile[s], lane);
             double e[G][4][2];
             tile_product<NR>(op, ring.tile[s], V, ring.zero, lane, e);
             const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;

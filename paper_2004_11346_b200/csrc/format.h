@@ -46,26 +46,38 @@ enum bf_op_flags {
     BF_OPF_REGEN = 4     /* `tile` is a seed block: regenerate the values (f1) */
 };
 
-/* Seed block of a regenerated dense tile (R rows, full 32-wide at most):
+/* Seed block of a regenerated dense tile (R rows, C <= 32 columns):
  *   double[0]: int32 first row r_a (index into x_pos), int32 unused
  *   double[1]: int64 offset (doubles) in the coefficient table of the step
  *              leaving the tile's first degree: alpha at [+0], beta at [+1],
  *              next step at [+2], [+3], ...
  *   double[2 + 3r .. 4 + 3r]: row r's p_prev, p_cur and exponent e (exact,
- *              as a double) at that degree
+ *              as a double) at the tile's first degree (column 0)
+ *   when C > 16, double[2 + 3R + 3r .. 4 + 3R + 3r]: the same state at
+ *              column 16 (the engine runs the two column halves as two
+ *              independent recurrence chains per row)
  * padded to a multiple of 16 doubles (128 B). */
+#define BF_SEED_SPLIT 16
 static inline
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-int64_t bf_seed_doubles(int R) {
-    return ((int64_t)(2 + 3 * R) + 15) / 16 * 16;
+int bf_seed_chains(int C) { return C > BF_SEED_SPLIT ? 2 : 1; }
+
+static inline
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+int64_t bf_seed_doubles(int R, int C) {
+    return ((int64_t)(2 + 3 * R * bf_seed_chains(C)) + 15) / 16 * 16;
 }
 
 typedef struct {
     int64_t tile;        /* element offset of the tile in the tile store  */
     int32_t in;          /* arena entry (contiguous) or idx offset (gather) */
-    int32_t aux;         /* lane-map index when BF_OPF_LANEMAP            */
+    int32_t aux;         /* lane-map index when BF_OPF_LANEMAP; recurrence-
+                            table offset of the tile's first step when
+                            BF_OPF_REGEN                                  */
     uint8_t kind, R, C, off;
     uint8_t flags, pad0;
     uint16_t pad1;

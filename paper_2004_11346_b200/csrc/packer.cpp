@@ -88,6 +88,7 @@ struct SeedJob {
     int h;            // half index (2 * order + parity)
     int r_a, R;       // rows
     int64_t c_a;      // first half column
+    int C;            // columns
 };
 
 struct TaskBuild {
@@ -344,6 +345,14 @@ struct Packer {
     // Regeneration choice for one tile of a turning block: full-height
     // tiles only (one recurrence chain per lane covers 32 rows), spread
     // evenly over the candidates in packing order.
+    // debugging knob: BFSHT_REGEN_COLS=full|partial restricts regeneration
+    // to full-width (32-column) or narrower tiles
+    static bool regen_cols_ok(int C) {
+        static const char *v = std::getenv("BFSHT_REGEN_COLS");
+        if (!v || !*v) return true;
+        return std::strcmp(v, "full") == 0 ? C == BF_T : C < BF_T;
+    }
+
     bool want_regen(int R) {
         if (M.regen <= 0.0 || R != BF_T) return false;
         const double f = M.regen >= 1.0 ? 1.0 : M.regen;
@@ -358,22 +367,30 @@ struct Packer {
             for (auto cc : cuts(c0, c1)) {
                 int R = (int)(rr.second - rr.first), C = (int)(cc.second - cc.first);
                 int flags = 0;
+                int32_t aux = 0;
                 int64_t t;
-                if (turning && want_regen(R)) {
+                if (turning && regen_cols_ok(C) && want_regen(R)) {
                     t = P.n_tiles;
-                    P.n_tiles += bf_seed_doubles(R);
-                    seeds.push_back({t, h_idx, (int)rr.first, R, cc.first});
+                    P.n_tiles += bf_seed_doubles(R, C);
+                    seeds.push_back({t, h_idx, (int)rr.first, R, cc.first, C});
                     flags = BF_OPF_REGEN;
                     P.n_regen++;
                     P.regen_values += (int64_t)R * C;
+                    // the engine stages the tile's step coefficients from
+                    // the rec table at issue time: their offset rides in aux
+                    const int o = h_idx / 2;
+                    const int64_t k_a = M.m[o] + (h_idx % 2 == 0 ? 1 : 0) + 2 * cc.first;
+                    const int64_t rb = rec_base[o] + 2 * (k_a - M.m[o]);
+                    if (rb > INT32_MAX) throw std::runtime_error("recurrence table exceeds int32 offsets");
+                    aux = (int32_t)rb;
                 } else {
                     t = alloc_tile(R, C, a + (rr.first - r0) * lda + (cc.first - c0), lda, 1);
                 }
                 int g = (int)(rr.first / BF_T), gc = (int)(cc.first / BF_T);
                 fwd_groups[h_idx][g].push_back(mk(BF_OP_TILE_N, t, hf.x + (int32_t)cc.first, R, C,
-                                                  (int)(rr.first - (int64_t)g * BF_T), flags));
+                                                  (int)(rr.first - (int64_t)g * BF_T), flags, aux));
                 inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, C,
-                                                   (int)(cc.first - (int64_t)gc * BF_T), flags));
+                                                   (int)(cc.first - (int64_t)gc * BF_T), flags, aux));
             }
     }
 
@@ -509,7 +526,7 @@ struct Packer {
                 const SeedJob &sj = seeds[j];
                 R = std::max(R, sj.R);
                 double *sb = T + sj.dst;
-                std::memset(sb, 0, sizeof(double) * bf_seed_doubles(sj.R));
+                std::memset(sb, 0, sizeof(double) * bf_seed_doubles(sj.R, sj.C));
                 const int64_t k_a = m + offset + 2 * sj.c_a;
                 int32_t hdr[2] = {sj.r_a, 0};
                 std::memcpy(sb, hdr, sizeof(hdr));
@@ -524,13 +541,17 @@ struct Packer {
                 int64_t k = m;
                 for (size_t j : js) {
                     const SeedJob &sj = seeds[j];
-                    const int64_t k_a = m + offset + 2 * sj.c_a;
-                    for (; k < k_a; ++k) bfr_step(xr, rec[2 * (k - m)], rec[2 * (k - m) + 1], &pp, &pc, &e);
-                    if (r < sj.R) {
-                        double *sr = T + sj.dst + 2 + 3 * r;
-                        sr[0] = pp;
-                        sr[1] = pc;
-                        sr[2] = (double)e;
+                    // chain starts: column 0, and column 16 when split
+                    for (int ch = 0; ch < bf_seed_chains(sj.C); ++ch) {
+                        const int64_t k_a = m + offset + 2 * (sj.c_a + ch * BF_SEED_SPLIT);
+                        for (; k < k_a; ++k)
+                            bfr_step(xr, rec[2 * (k - m)], rec[2 * (k - m) + 1], &pp, &pc, &e);
+                        if (r < sj.R) {
+                            double *sr = T + sj.dst + 2 + 3 * (ch * sj.R + r);
+                            sr[0] = pp;
+                            sr[1] = pc;
+                            sr[2] = (double)e;
+                        }
                     }
                 }
             }
@@ -1067,7 +1088,9 @@ extern "C" int bfsht_rec_coeffs(int64_t m, int64_t k_max, double *out) {
     return 0;
 }
 
-// Host twin of the engine's tile generation (engine.cu regen_tile).
+// Host twin of the engine's tile generation (engine.cu regen_tile): each
+// chain (columns [0, 16) and [16, C)) re-runs the reference step sequence
+// (bfr_step, range test after every step) from its own seed.
 extern "C" int bfsht_regen_tile_host(const double *seed, int R, int C, const double *rec,
                                      const double *x_pos, double mag_min, double *out) {
     if (!seed || !rec || !x_pos || !out || R < 1 || R > BF_T || C < 1 || C > BF_T) return -1;
@@ -1076,18 +1099,22 @@ extern "C" int bfsht_regen_tile_host(const double *seed, int R, int C, const dou
     int64_t rb;
     std::memcpy(&rb, seed + 1, sizeof(rb));
     const int C4 = (C + 3) / 4;
+    const int K = bf_seed_chains(C);
     std::memset(out, 0, sizeof(double) * bf_tile_doubles(R, C));
     for (int r = 0; r < R; ++r) {
-        double pp = seed[2 + 3 * r], pc = seed[3 + 3 * r];
-        int e = (int)seed[4 + 3 * r];
         const double xr = x_pos[hdr[0] + r];
-        for (int c = 0; c < C; ++c) {
-            double v = std::ldexp(pc, e);
-            if (std::fabs(v) < mag_min) v = 0.0;
-            out[bf_tile_index(r, c, C4)] = v;
-            if (c + 1 < C) {
-                bfr_step(xr, rec[rb + 4 * c], rec[rb + 4 * c + 1], &pp, &pc, &e);
-                bfr_step(xr, rec[rb + 4 * c + 2], rec[rb + 4 * c + 3], &pp, &pc, &e);
+        for (int ch = 0; ch < K; ++ch) {
+            const int c0 = ch * BF_SEED_SPLIT, c1 = (ch + 1 < K) ? c0 + BF_SEED_SPLIT : C;
+            double pp = seed[2 + 3 * (ch * R + r)], pc = seed[3 + 3 * (ch * R + r)];
+            int e = (int)seed[4 + 3 * (ch * R + r)];
+            for (int c = c0; c < c1; ++c) {
+                double v = std::ldexp(pc, e);
+                if (std::fabs(v) < mag_min) v = 0.0;
+                out[bf_tile_index(r, c, C4)] = v;
+                if (c + 1 < c1) {
+                    bfr_step(xr, rec[rb + 4 * c], rec[rb + 4 * c + 1], &pp, &pc, &e);
+                    bfr_step(xr, rec[rb + 4 * c + 2], rec[rb + 4 * c + 3], &pp, &pc, &e);
+                }
             }
         }
     }

@@ -128,7 +128,8 @@ class PackedPlan:
             return 0
         tiles, first = np.unique(self.ops["tile"][sel], return_index=True)
         rows = self.ops["R"][sel][first].astype(np.int64)
-        return int(np.sum((2 + 3 * rows + 15) // 16 * 16))
+        chains = np.where(self.ops["C"][sel][first] > 16, 2, 1)   # format.h bf_seed_chains
+        return int(np.sum((2 + 3 * rows * chains + 15) // 16 * 16))
 
     @property
     def n(self):
@@ -161,7 +162,7 @@ class PackedPlan:
 # Planning N=1024 takes seconds here but the reference needs minutes (hours
 # at N=4096); a cached plan skips planning and packing entirely.
 _PK_MAGIC = b"BFPK"
-_PK_VERSION = 1
+_PK_VERSION = 2   # 2: two-chain regeneration seed blocks
 _PK_ALIGN = 4096
 _PK_FIELDS = ("tiles", "ops", "idx", "maps", "tasks", "halves", "stages_fwd",
               "stages_inv", "rec", "xpos", "flow", "tinfo")
