@@ -50,6 +50,7 @@ struct bfsht_plan {
     int32_t *dft_perm = nullptr;      // digit-reversal positions
     double *dft_tw = nullptr;         // L complex: exp(i m phi0) per bin
     std::vector<int32_t> dft_radix;
+    int dft_gen = 0;                  // generic-radix staging bytes (dynamic smem tail)
     double *dft_scratch = nullptr;    // global fallback buffer
     int64_t dft_scratch_rows = 0;
     int64_t launches = 0;

@@ -129,27 +129,144 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
     }
 }
 
-// generic radix (large primes), local-memory arrays
-__device__ void butterfly_any(double2 *row, int base, int span, int k, int P, const double2 *Tw,
-                              const double2 *__restrict__ R, bool inv) {
-    double2 x[128];
-    for (int q = 0; q < P; ++q) {
-        x[q] = row[base + q * span];
-        if (q > 0 && span > 1) x[q] = cmul(x[q], conjif(Tw[(q - 1) * span + k], inv));
+// Generic prime radix P (17 <= P <= 255; the 43 and 127 of N=4096's
+// L = 16383, the 31 and 151 of N=8192's L = 32767) as a whole-CTA pass over
+// batches of butterflies.  The batch's inputs (inter-pass twiddles
+// applied) are staged in shared memory in the conjugate-pair form
+// a_j = x_j + x_{P-j}, b_j = x_j - x_{P-j}; a thread then forms RS output
+// pairs (s, P-s) of RB butterflies,
+//   y_s, y_{P-s} = x_0 + sum_j a_j cos(2 pi js/P) +- i sum_j b_j sin(..),
+// so each shared load of a root or of an a_j/b_j feeds several FMAs (the
+// first version, one output pair per thread, was shared-load bound).
+// Staging lives at the end of the dynamic shared memory (kGenBytes, added
+// to the launch only when the length has such a radix).
+constexpr int kGenMaxP = 255;
+constexpr int kGenCap = 2048;                       // staged (a, b) items
+constexpr int kGenRootsDoubles = 512;               // cos / sin of <= 256 roots
+constexpr int kGenBytes = kGenRootsDoubles * 8 + 2 * kGenCap * 16;
+constexpr int kGenRS = 2, kGenRB = 4;
+
+__device__ __forceinline__ double *gen_staging() {
+    extern __shared__ __align__(16) double2 dsm[];
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    return reinterpret_cast<double *>(reinterpret_cast<char *>(dsm) + dyn - kGenBytes);
+}
+
+__device__ void generic_pass(double2 *buf, int nrows, int L, int span, int P, const double2 *Tw,
+                             const double2 *__restrict__ R, bool inv) {
+    double *g = gen_staging();
+    double *s_cr = g, *s_ci = g + kGenRootsDoubles / 2;
+    double2 *s_a = reinterpret_cast<double2 *>(g + kGenRootsDoubles), *s_b = s_a + kGenCap;
+    const int H = (P - 1) / 2, W = H + 1;
+    const int NB = (kGenCap / W) / kGenRB * kGenRB;   // butterflies per batch
+    const int NQ = NB / kGenRB, NSG = (H + kGenRS - 1) / kGenRS;
+    for (int t = threadIdx.x; t < P; t += blockDim.x) {
+        const double2 w = R[t];
+        s_cr[t] = w.x;
+        s_ci[t] = inv ? -w.y : w.y;
     }
-    for (int s = 0; s < P; ++s) {
-        double2 acc = x[0];
-        for (int q = 1; q < P; ++q) {
-            double2 t = cmul(x[q], conjif(R[(q * s) % P], inv));
-            acc.x += t.x;
-            acc.y += t.y;
+    const int nb = L / P, total = nb * nrows;
+    for (int g0 = 0; g0 < total; g0 += NB) {
+        __syncthreads();   // roots written / previous batch's staging consumed
+        // staging, item = j * NB + bi: consecutive threads take consecutive
+        // butterflies (consecutive k), so the loads coalesce when span > 1
+        for (int it = threadIdx.x; it < NB * W; it += blockDim.x) {
+            const int j = it / NB, bi = it - j * NB, gi = g0 + bi;
+            if (gi >= total) continue;
+            const int rw = gi >= nb ? gi / nb : 0, tt = gi - rw * nb;
+            const int gg = tt / span, k = tt - gg * span;
+            const double2 *row = buf + (int64_t)rw * L + gg * span * P + k;
+            double2 xj = row[j * span];
+            if (j > 0 && span > 1) xj = cmul(xj, conjif(Tw[(j - 1) * span + k], inv));
+            if (j == 0) {
+                s_a[bi] = xj;
+                s_b[bi] = make_double2(0.0, 0.0);
+            } else {
+                double2 xm = row[(P - j) * span];
+                if (span > 1) xm = cmul(xm, conjif(Tw[(P - j - 1) * span + k], inv));
+                s_a[j * NB + bi] = make_double2(xj.x + xm.x, xj.y + xm.y);
+                s_b[j * NB + bi] = make_double2(xj.x - xm.x, xj.y - xm.y);
+            }
         }
-        row[base + s * span] = acc;
+        __syncthreads();
+        // y_0 of every butterfly
+        for (int bi = threadIdx.x; bi < NB; bi += blockDim.x) {
+            const int gi = g0 + bi;
+            if (gi >= total) continue;
+            const int rw = gi >= nb ? gi / nb : 0, tt = gi - rw * nb;
+            const int gg = tt / span, k = tt - gg * span;
+            double2 y0 = s_a[bi];
+            for (int j = 1; j <= H; ++j) {
+                y0.x += s_a[j * NB + bi].x;
+                y0.y += s_a[j * NB + bi].y;
+            }
+            buf[(int64_t)rw * L + gg * span * P + k] = y0;
+        }
+        // output pairs: item = bq + NQ * sg, RS pairs x RB butterflies
+        // bi = r * NQ + bq; staging is j-major (entry j * NB + bi), so a
+        // warp's loads of one (j, r) hit consecutive 16-byte entries
+        for (int it = threadIdx.x; it < NQ * NSG; it += blockDim.x) {
+            const int sg = it / NQ, bq = it - sg * NQ;
+            const int s0 = 1 + sg * kGenRS;
+            double2 re[kGenRS][kGenRB], im[kGenRS][kGenRB];
+#pragma unroll
+            for (int r = 0; r < kGenRB; ++r) {
+                const double2 x0 = s_a[r * NQ + bq];
+#pragma unroll
+                for (int q = 0; q < kGenRS; ++q) {
+                    re[q][r] = x0;
+                    im[q][r] = make_double2(0.0, 0.0);
+                }
+            }
+            int t[kGenRS];
+#pragma unroll
+            for (int q = 0; q < kGenRS; ++q) t[q] = 0;
+            for (int j = 1; j <= H; ++j) {
+                double c[kGenRS], sn[kGenRS];
+#pragma unroll
+                for (int q = 0; q < kGenRS; ++q) {
+                    t[q] += s0 + q;
+                    if (t[q] >= P) t[q] -= P;
+                    c[q] = s_cr[t[q]];
+                    sn[q] = s_ci[t[q]];
+                }
+#pragma unroll
+                for (int r = 0; r < kGenRB; ++r) {
+                    const double2 A = s_a[j * NB + r * NQ + bq];
+                    const double2 B = s_b[j * NB + r * NQ + bq];
+#pragma unroll
+                    for (int q = 0; q < kGenRS; ++q) {
+                        re[q][r].x = fma(A.x, c[q], re[q][r].x);
+                        re[q][r].y = fma(A.y, c[q], re[q][r].y);
+                        im[q][r].x = fma(B.x, sn[q], im[q][r].x);
+                        im[q][r].y = fma(B.y, sn[q], im[q][r].y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < kGenRB; ++r) {
+                const int gi = g0 + r * NQ + bq;
+                if (gi >= total) continue;
+                const int rw = gi >= nb ? gi / nb : 0, tt = gi - rw * nb;
+                const int gg = tt / span, k = tt - gg * span;
+                double2 *row = buf + (int64_t)rw * L + gg * span * P + k;
+#pragma unroll
+                for (int q = 0; q < kGenRS; ++q) {
+                    const int sidx = s0 + q;
+                    if (sidx > H) continue;
+                    row[sidx * span] = make_double2(re[q][r].x - im[q][r].y, re[q][r].y + im[q][r].x);
+                    row[(P - sidx) * span] =
+                        make_double2(re[q][r].x + im[q][r].y, re[q][r].y - im[q][r].x);
+                }
+            }
+        }
     }
 }
 
 // All passes over `nrows` rows of buf (row stride L), whole CTA.  Tw: the
 // pass twiddle table (L entries, shared or global memory); R: radix roots.
+template <bool GEN = true>
 __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const double2 *Tw,
                            const double2 *__restrict__ R, bool inv) {
     const int L = d.L;
@@ -166,14 +283,9 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const doub
             case 7: radix_pass<7>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 11: radix_pass<11>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 13: radix_pass<13>(buf, nrows, L, span, si, tw, rr, inv); break;
-            default: {
-                const int nb = L / P;
-                for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
-                    const int rw = t / nb, tt = t - rw * nb;
-                    const int k = tt % span, g = tt / span;
-                    butterfly_any(buf + (int64_t)rw * L, g * span * P + k, span, k, P, tw, rr, inv);
-                }
-            }
+            default:
+                if (GEN) generic_pass(buf, nrows, L, span, P, tw, rr, inv);
+                else __trap();   // launched without the generic radix (host picks by radices)
         }
         __syncthreads();
         span *= P;
@@ -190,7 +302,7 @@ __device__ __forceinline__ double2 *dft_buffer(double2 *scratch, int rows, int L
 }
 
 // ---- standalone batched DFT: rows of length L (numpy fft / L*ifft)
-template <bool SM>
+template <bool SM, bool GEN>
 __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
     DftDesc d, const double2 *__restrict__ in, double2 *__restrict__ out, int64_t rows,
     const int *__restrict__ perm, const double2 *__restrict__ W, bool inv, bool use_smem,
@@ -201,7 +313,7 @@ __global__ void __launch_bounds__(kDftThreads) dft_rows_kernel(
         const double2 *src = in + rw * L;
         for (int j = threadIdx.x; j < L; j += blockDim.x) buf[perm[j]] = src[j];
         __syncthreads();
-        dft_passes(buf, 1, d, W, W + L, inv);
+        dft_passes<GEN>(buf, 1, d, W, W + L, inv);
         double2 *dst = out + rw * L;
         for (int j = threadIdx.x; j < L; j += blockDim.x) dst[j] = buf[j];
         __syncthreads();
@@ -590,15 +702,21 @@ DftDesc make_desc(const bfsht_plan *pl) {
 
 int dft_smem_bytes(int64_t L, int rows) { return (int)(rows * L * 16); }
 
-// two rows + the twiddle table when that fits the 227 KB opt-in limit
-bool dft_w_smem(int64_t L) { return 3 * L * 16 <= 227 * 1024; }
-int dft_pair_smem(int64_t L) { return dft_smem_bytes(L, dft_w_smem(L) ? 3 : 2); }
-// analysis kernel: + node-half bases (int32 per half) when they fit too
-bool dft_y_smem(int64_t L, int64_t nh) {
-    return dft_w_smem(L) && 3 * L * 16 + 4 * nh <= 227 * 1024;
+// generic-radix staging bytes of a factorization (0 when every radix is templated)
+int dft_gen_bytes(const std::vector<int> &rad) {
+    for (int p : rad)
+        if (p > 13) return kGenBytes;
+    return 0;
 }
-int dft_anal_smem(int64_t L, int64_t nh) {
-    return dft_pair_smem(L) + (dft_y_smem(L, nh) ? (int)(4 * nh) : 0);
+// shared-memory layouts (bytes); gen = the generic-radix staging at the tail
+bool dft_w_smem(int64_t L, int gen) { return 3 * L * 16 + gen <= 227 * 1024; }
+int dft_pair_smem(int64_t L, int gen) { return dft_smem_bytes(L, dft_w_smem(L, gen) ? 3 : 2) + gen; }
+// analysis kernel: + node-half bases (int32 per half) when they fit too
+bool dft_y_smem(int64_t L, int64_t nh, int gen) {
+    return dft_w_smem(L, gen) && 3 * L * 16 + 4 * nh + gen <= 227 * 1024;
+}
+int dft_anal_smem(int64_t L, int64_t nh, int gen) {
+    return dft_pair_smem(L, gen) + (dft_y_smem(L, nh, gen) ? (int)(4 * nh) : 0);
 }
 
 }  // namespace
@@ -627,8 +745,8 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         }
     }
     for (int p : rad)
-        if (p > 128) {
-            bfsht_set_error("DFT length has a prime factor above 128 (needs Bluestein)");
+        if (p > kGenMaxP) {
+            bfsht_set_error("DFT length has a prime factor above 256 (needs Bluestein)");
             return -4;
         }
     std::vector<double> w(2 * L), tw(2 * L), wt;
@@ -684,19 +802,30 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     BF_CUDA(cudaMemcpy(pl->dft_perm, perm.data(), 4 * L, cudaMemcpyHostToDevice));
     pl->dft_radix = rad;
     pl->dft_L = L;
+    pl->dft_gen = dft_gen_bytes(rad);
+    const int gen = pl->dft_gen;
     const int need = dft_smem_bytes(L, 2);
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
-    if (need > maxsm) {
+    if (gen > 0) {
+        // global-scratch variants: their dynamic shared memory is the staging
+        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
+        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
+        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
+    }
+    if (need + gen > maxsm) {
         const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
         BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * L * rows));
         pl->dft_scratch_rows = rows;
     } else {
-        const int pair = dft_pair_smem(L);
+        const int pair = dft_pair_smem(L, gen);
         BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
         BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     std::max(pair, dft_anal_smem(L, 2 * (int64_t)pl->norders))));
-        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, need));
+                                     std::max(pair, dft_anal_smem(L, 2 * (int64_t)pl->norders, gen))));
+        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     std::min(dft_smem_bytes(L, 1) + gen, 227 * 1024)));
+        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     dft_smem_bytes(L, 1)));
     }
     return 0;
 }
@@ -719,10 +848,10 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), pl->info[10],
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), pl->info[10],
         2 * pl->norders, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -738,11 +867,11 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     const int64_t nh = 2 * (int64_t)pl->norders;
-    const bool ysm = sm && dft_y_smem(pl->dft_L, nh);
-    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(pl->dft_L, nh) : dft_pair_smem(pl->dft_L)) : 0, st>>>(
+    const bool ysm = sm && dft_y_smem(pl->dft_L, nh, pl->dft_gen);
+    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(pl->dft_L, nh, pl->dft_gen) : dft_pair_smem(pl->dft_L, pl->dft_gen)) : pl->dft_gen, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L),
+        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen),
         ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -967,26 +1096,26 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
         rc = bf_alt_apply_wide(pl, BFSHT_FORWARD, work, st);
         if (rc) return rc;
         for (int b = 0; b < B; ++b) {
-            (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(L) : 0, st>>>(
+            (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(L, pl->dft_gen) : pl->dft_gen, st>>>(
                 d, n, pl->layout_fwd, work + BF_NRHS * b, 0, n,
                 reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<double2 *>(out) + b * ngrid, sm,
-                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L), pl->info[10],
+                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen), pl->info[10],
                 2 * pl->norders, ew);
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
         }
     } else {
         const int64_t nh = 2 * (int64_t)pl->norders;
-        const bool ysm = sm && dft_y_smem(L, nh);
+        const bool ysm = sm && dft_y_smem(L, nh, pl->dft_gen);
         for (int b = 0; b < B; ++b) {
-            (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(L, nh) : dft_pair_smem(L)) : 0, st>>>(
+            (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(L, nh, pl->dft_gen) : dft_pair_smem(L, pl->dft_gen)) : pl->dft_gen, st>>>(
                 d, n, pl->layout_inv, work + BF_NRHS * b,
                 reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<const double2 *>(in) + b * ngrid, weights, 0, n, sm,
-                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L),
+                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen),
                 ysm ? pl->node_y : nullptr, (int)nh, ew);
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
@@ -1007,11 +1136,15 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
                 cudaStream_t st) {
     int rc = bf_dft_prepare(pl, L);
     if (rc) return rc;
-    const bool sm = dft_smem_bytes(L, 1) <= 227 * 1024 && pl->dft_scratch == nullptr;
+    const bool sm = dft_smem_bytes(L, 1) + pl->dft_gen <= 227 * 1024 && pl->dft_scratch == nullptr;
     int grid = (int)(rows < 4096 ? rows : 4096);
     if (!sm) grid = (int)std::min<int64_t>(grid, pl->dft_scratch_rows);
     if (grid <= 0) return 0;
-    (sm ? dft_rows_kernel<true> : dft_rows_kernel<false>)<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) : 0, st>>>(
+    // kernels without the generic-radix code keep the smaller register
+    // footprint (2 CTAs per SM) for the all-templated lengths
+    auto kern = sm ? (pl->dft_gen ? dft_rows_kernel<true, true> : dft_rows_kernel<true, false>)
+                   : (pl->dft_gen ? dft_rows_kernel<false, true> : dft_rows_kernel<false, false>);
+    kern<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) + pl->dft_gen : pl->dft_gen, st>>>(
         make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
@@ -1028,11 +1161,11 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), (int64_t)0, 0, BF_NRHS);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), (int64_t)0, 0, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -1046,11 +1179,11 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L) : 0, st>>>(
+    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L), nullptr, 0, BF_NRHS);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), nullptr, 0, BF_NRHS);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;

@@ -32,6 +32,11 @@ x = torch.randn(2 * n, L, dtype=torch.complex128, device="cuda")
 out = {"tag": os.environ.get("BFSHT_NVCC_FLAGS", "")}
 out["dft_rows_fwd_ms"] = timed(lambda: dft_rows(x))
 out["dft_rows_inv_ms"] = timed(lambda: dft_rows(x, inverse=True))
+del x
+for LL, rows in ((16383, 16384), (32767, 2048)):
+    xl = torch.randn(rows, LL, dtype=torch.complex128, device="cuda")
+    out[f"dft_rows_L{LL}_x{rows}_ms"] = timed(lambda: dft_rows(xl), reps=3)
+    del xl
 plans = plan_orders(n, range(2 * n), SamplingConfig(tolerance=1e-12), processes=0)
 dp = DevicePlan(plans)
 c = torch.from_numpy(synthetic_coeffs(n)).cuda()

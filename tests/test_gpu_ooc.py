@@ -63,12 +63,13 @@ def test_chunked_sht_matches_oracle(n, chunks, reserve):
     run.close()
 
 
-def test_dft_rows_l16383():
-    # the N=4096 row length (4N-1 = 16383 = 3 * 43 * 127) does not fit the
-    # shared-memory DFT path; the global-scratch variant runs instead
+@pytest.mark.parametrize("L", [16383, 32767])
+def test_dft_rows_large_prime_radices(L):
+    # the N=4096 / N=8192 row lengths (4N-1 = 3 * 43 * 127 / 7 * 31 * 151)
+    # do not fit the shared-memory DFT path (the global-scratch variant runs)
+    # and have prime radices above 13 (the cooperative generic pass)
     import torch
     from paper_2004_11346_b200.api import dft_rows
-    L = 16383
     rng = np.random.default_rng(L)
     x = rng.standard_normal((5, L)) + 1j * rng.standard_normal((5, L))
     xt = torch.from_numpy(x).cuda()
