@@ -296,21 +296,6 @@ __device__ __forceinline__ long long abits(double v) {
     return (long long)(((unsigned long long)hi << 32) | lo);
 }
 
-// ldexp(p, e) flushed to 0 below mag_min (recur.c emit), branch-free on the
-// integer pipe: a normal p with a normal result only shifts its exponent
-// field (exact); a result below 2^-1022 is under mag_min (~2^-1010) and
-// flushes anyway; p = 0 gives 0.  (p is never subnormal or huge here: the
-// mantissas stay within [2^-560, 2^560] or are exactly 0, see regen_tile.)
-// The flush compares magnitudes as IEEE bit patterns, which orders finite
-// values exactly like the floating-point compare.
-__device__ __forceinline__ double emit_value(double p, int e, long long mag_bits) {
-    const long long b = __double_as_longlong(p);
-    const int ef = (int)(((unsigned)__double2hiint(p) >> 20) & 0x7ffu);
-    const long long v = (ef != 0 && ef + e >= 1) ? b + ((long long)e << 52) : 0LL;
-    const double d = __longlong_as_double(v);
-    return abits(d) < mag_bits ? 0.0 : d;
-}
-
 // One recurrence step without the range test (recur.h bfr_step's
 // arithmetic: three roundings, one subtraction, no FMA).
 __device__ __forceinline__ void rec_step(double x, double a, double b, double &pp, double &pc) {
