@@ -82,9 +82,6 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
         ci[t] = inv ? -w.y : w.y;
     }
     const int nb = L / P;
-    // small radices: two butterflies per thread in flight (independent
-    // loads / products) to cover shared-memory latency at 8 warps per SM
-#pragma unroll (P <= 7 ? 2 : 1)
     for (int t = threadIdx.x; t < nb * nrows; t += blockDim.x) {
         // nrows <= 2: the row by one compare, the group by a multiply-high
         const int rw = t >= nb ? 1 : 0, tt = t - rw * nb;
