@@ -57,7 +57,7 @@ struct Width {
     static constexpr int G = NR >= 8 ? NR / 8 : 1;      // n-groups
     static constexpr int QACT = NR >= 8 ? 4 : NR / 2;   // lanes q < QACT own RHS
     static constexpr int GACT = NR >= 8 ? 8 : NR;       // valid B columns
-    static constexpr int WARPS = NR == 4 ? kWarps : 8;  // register / shared-memory bound
+    static constexpr int WARPS = NR == 4 ? kWarps : (kStages == 2 ? 8 : (kStages == 3 ? 5 : 4));  // register / shared-memory bound
 };
 
 template <int NR>

@@ -17,8 +17,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--tol", type=float, default=1e-12)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--chunk", type=int, default=0,
+                help="plan only chunk 0 of this many LPT chunks (N=4096-style runs)")
 a = ap.parse_args()
-plans = plan_orders(a.n, range(2 * a.n), SamplingConfig(tolerance=a.tol), processes=0)
+if a.chunk:
+    from paper_2004_11346_b200.dist import lpt_orders
+    orders = lpt_orders(a.n, a.chunk)[0]
+else:
+    orders = range(2 * a.n)
+plans = plan_orders(a.n, orders, SamplingConfig(tolerance=a.tol), processes=0)
 dp = DevicePlan(plans)
 pk = dp.packed
 ops, tasks = pk.ops, pk.tasks
