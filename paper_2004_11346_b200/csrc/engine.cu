@@ -321,25 +321,6 @@ __device__ __forceinline__ void rec_rescale(double &pp, double &pc, int &e) {
     e += big ? 1000 : (small ? -1000 : 0);
 }
 
-// Regenerate a dense turning tile in place from its seed block:
-// lane r re-runs row r's degree recurrence as the planner did (recur.h;
-// pkg/src/bfsht/kernels/_recur_cy.pyx:45-66), two steps per column
-// (degrees of one parity), emitting ldexp(p, e) flushed below MAG_MIN —
-// the stored values bit for bit (tests/test_regen_pack.py,
-// tests/test_gpu_regen.py).
-//
-// Cost shape (measured: the first version spent ~2500 warp instructions
-// per tile, latency-bound on branches and per-step range tests): the
-// reference tests the (mantissa, 2^e) range after every step; here it is
-// tested once per 4 columns (8 steps), branch-free.  The rescale multiplies
-// by an exact power of two; a step grows |p| by at most alpha |x| + beta
-// < 2^7 and shrinks the larger of |p_k|, |p_k-1| by at most ~2, so between
-// tests the mantissas stay inside [2^-510, 2^556] (a nonzero difference of
-// two rounded products there is above 2^-560): every intermediate is the
-// reference's value times 2^(1000 j), and every emitted ldexp(p, e) is the
-// same number.  Step coefficients (alpha, beta of the column's two steps)
-// are a warp-uniform 32-byte load per column, issued a column ahead.
-// Padding rows / columns come out as zeros (padding lanes run x = p = 0).
 // One block step of K chains (chain h covers columns [16h, ...)): emit
 // column block j of each chain, advance each by its 4 columns, range-test.
 // Emission with e fixed for the block, as one 64-bit compare: for a value
