@@ -95,7 +95,8 @@ class ChunkedSht:
     chunk (default: ``plan_orders`` in ``processes`` host processes)."""
 
     def __init__(self, n, nchunks, params=None, tau=None, n0=None, processes=0,
-                 planner=None, reserve_bytes=24 << 30, device=None, verbose=False):
+                 planner=None, reserve_bytes=24 << 30, device=None, verbose=False,
+                 only=None):
         import torch
         from .api import DevicePlan
         from .legendre import gauss_legendre
@@ -114,6 +115,11 @@ class ChunkedSht:
         self.planner = planner
         self.reserve_bytes = int(reserve_bytes)
         self.verbose = verbose
+        # only: chunk indices to process (None = all).  A subset runs the
+        # full-size grid and DFT stage with the other orders' node halves
+        # zero: the transform of coefficients supported on those orders
+        # (a sampled run when the whole plan is out of reach, e.g. N=8192).
+        self.only = None if only is None else sorted(set(int(c) for c in only))
         self.chunks, self.layout, self.block, entries = chunk_layout(n, self.nchunks)
         dev = self.device
         self.ybuf = torch.zeros((entries, NRHS), dtype=torch.float64, device=dev)
@@ -210,10 +216,14 @@ class ChunkedSht:
         grid: device (2N, 4N-1) complex128.  Returns a report dict."""
         torch, lib = self.torch, self.lib
         n = self.n
+        if self.only is not None:
+            self.ybuf.zero_()   # orders outside the subset contribute nothing
         self._events = []
         rep = {"plan_s": 0.0, "pack_upload_s": 0.0, "alt_bytes": 0, "payload_values": 0,
                "chunks": []}
         for c, orders in enumerate(self.chunks):
+            if self.only is not None and c not in self.only:
+                continue
             dp, tp, tu = self._chunk_plan(c)
             rep["plan_s"] += tp
             rep["pack_upload_s"] += tu
@@ -264,7 +274,9 @@ class ChunkedSht:
         out = np.zeros(4 * n * n, dtype=np.complex128)
         rep = {"plan_s": 0.0, "pack_upload_s": 0.0, "alt_bytes": 0, "payload_values": 0,
                "chunks": [], "replanned": 0}
-        order = sorted(range(len(self.chunks)), key=lambda c: c not in self.resident)
+        order = sorted((c for c in range(len(self.chunks))
+                        if self.only is None or c in self.only),
+                       key=lambda c: c not in self.resident)
         for c in order:
             orders = self.chunks[c]
             replan = c not in self.resident

@@ -38,6 +38,13 @@ def main():
     ap.add_argument("--rows", default="0,1000,4095")
     ap.add_argument("--reserve-gb", type=float, default=24.0)
     ap.add_argument("--out", default="gpurun_out/ooc_n{n}.json")
+    ap.add_argument("--only", default="",
+                    help="process only these chunks (comma list): a sampled run "
+                         "through the full grid and DFT stage (N=8192)")
+    ap.add_argument("--decay", type=float, default=1.0,
+                    help="coefficient spectrum (1+k)^-decay (config 5: 2)")
+    ap.add_argument("--real-grid", action="store_true",
+                    help="also time an inverse of a real iid U(-1,1) grid (config 5)")
     args = ap.parse_args()
 
     import torch
@@ -51,9 +58,24 @@ def main():
     L = 4 * n - 1
     params = SamplingConfig(tolerance=args.tol)
     t0 = time.perf_counter()
+    only = [int(v) for v in args.only.split(",") if v] or None
     run = ChunkedSht(n, args.chunks, params=params, processes=args.procs,
-                     reserve_bytes=int(args.reserve_gb * (1 << 30)), verbose=True)
-    flat = synthetic_coeffs(n, seed=3)
+                     reserve_bytes=int(args.reserve_gb * (1 << 30)), verbose=True, only=only)
+    _, offs0 = OA.coeff_offsets(n)
+    if only is None and args.decay == 1.0:
+        flat = synthetic_coeffs(n, seed=3)
+        subset = None
+    else:
+        # coefficients (iid N(0,1) (1+k)^-decay) on the processed orders only
+        subset = sorted(m for c in (only or range(len(run.chunks))) for m in run.chunks[c])
+        flat = np.zeros(int(offs0[-1]), dtype=np.complex128)
+        rng = np.random.default_rng(3)
+        for m in subset:
+            for mm in ((m, -m) if m else (m,)):
+                i = (2 * n - 1) + mm
+                k = np.arange(abs(mm), 2 * n, dtype=np.float64)
+                flat[offs0[i]:offs0[i + 1]] = (rng.standard_normal(k.size)
+                                               + 1j * rng.standard_normal(k.size)) / (1.0 + k) ** args.decay
     grid = torch.empty((2 * n, L), dtype=torch.complex128, device="cuda")
     fwd = run.forward(flat, grid)
     print(f"forward: device {fwd['device_ms']:.1f} ms (ALT {fwd['alt_ms']:.1f} ms, "
@@ -61,6 +83,9 @@ def main():
           f"pack+upload {fwd['pack_upload_s']:.0f} s", file=sys.stderr, flush=True)
 
     samples = [int(v) for v in args.samples.split(",") if v]
+    if subset is not None:
+        samples = [m for m in samples if m in set(subset)] or \
+            [subset[0], subset[len(subset) // 2], subset[-1]]
     checks = {}
     _, offs = OA.coeff_offsets(n)
     plans = {}
@@ -118,7 +143,13 @@ def main():
           f"{inv['alt_gbs']:.0f} GB/s), plan {inv['plan_s']:.0f} s (replanned "
           f"{inv['replanned']} chunks)", file=sys.stderr, flush=True)
     back = inv.pop("coeffs")
-    checks["roundtrip_rel_l2"] = float(np.linalg.norm(back - flat) / np.linalg.norm(flat))
+    if subset is None:
+        checks["roundtrip_rel_l2"] = float(np.linalg.norm(back - flat) / np.linalg.norm(flat))
+    else:
+        sel = np.concatenate([np.arange(offs0[(2 * n - 1) + mm], offs0[(2 * n - 1) + mm + 1])
+                              for m in subset for mm in ((m, -m) if m else (m,))])
+        checks["roundtrip_rel_l2"] = float(np.linalg.norm(back[sel] - flat[sel])
+                                           / np.linalg.norm(flat[sel]))
     # inverse of sampled orders from the GPU grid's spectrum columns
     errs = []
     jj = np.arange(L)
@@ -163,6 +194,34 @@ def main():
             errs.append(float(np.linalg.norm(got - want) / np.linalg.norm(want)))
     checks["alt_inverse_vs_oracle_max"] = max(errs)
 
+    real_inv = None
+    if args.real_grid:
+        # config 5's inverse input: a real grid, iid U(-1,1), promoted to
+        # complex (sht.py:151-166)
+        g = torch.from_numpy(np.random.default_rng(5).uniform(-1.0, 1.0, (2 * n, L))) \
+            .to(torch.complex128).cuda()
+        real_inv = run.inverse(g)
+        rb = real_inv.pop("coeffs")
+        errs = []
+        for m in samples:
+            p = plans[m]
+            e = run.node_entries(m)
+            for sgn, cols in ((1, (0, 1)), (-1, (2, 3))):
+                if m == 0 and sgn < 0:
+                    continue
+                want = np.zeros(2 * n - m, dtype=np.complex128)
+                for par, spec, blocks, sl in ((0, p.spec_odd, p.blocks_odd, slice(1, None, 2)),
+                                              (1, p.spec_even, p.blocks_even, slice(0, None, 2))):
+                    if spec is None:
+                        continue
+                    want[sl] = OA.apply_half_transpose(blocks, e[par][:, cols[0]], spec.num_cols) \
+                        + 1j * OA.apply_half_transpose(blocks, e[par][:, cols[1]], spec.num_cols)
+                i = (2 * n - 1) + sgn * m
+                got = rb[offs[i]:offs[i + 1]]
+                errs.append(float(np.linalg.norm(got - want) / np.linalg.norm(want)))
+        checks["real_grid_alt_inverse_vs_oracle_max"] = max(errs)
+        print(f"real-grid inverse: device {real_inv['device_ms']:.1f} ms", file=sys.stderr, flush=True)
+
     v_n = fwd["payload_values"]
     dev_ms = fwd["device_ms"] + inv["device_ms"]
     res = {
@@ -184,6 +243,17 @@ def main():
         "samples": samples,
         "alt_ms_per_chunk_fwd": fwd["alt_ms_per_chunk"],
     }
+    if only is not None:
+        res["workload"] = (f"C5-style sampled run: N={n}, tol {args.tol:g}, one B200, chunks {only} "
+                           f"of {len(run.chunks)} ({len(subset)} orders, coefficients (1+k)^-"
+                           f"{args.decay:g} on them, zero elsewhere) through the full "
+                           f"{2 * n} x {L} grid and DFT stage")
+        res["orders_processed"] = len(subset)
+        res["note"] = ("device_ms / transforms_per_s cover the processed chunks' ALT plus the "
+                       "full-grid DFT stage; not a whole-plan number")
+    if real_inv is not None:
+        res["real_grid_inverse_device_ms"] = real_inv["device_ms"]
+        res["real_grid_inverse_dft_ms"] = real_inv["dft_ms"]
     if cpu["values"]:
         res["cpu_baseline"] = {
             "kind": "port", "cores": 1,
