@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kDftThreads, 2) dft_rows_kernel(
 
 // ---- forward SHT: node halves -> assembled rows -> L*ifft -> grid rows
 template <bool SM>
-__global__ void __launch_bounds__(kDftThreads, SM ? 1 : 2) sht_synth_kernel(
+__global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kDftThreads, SM ? 1 : 2) sht_synth_kernel(
 
 // ---- inverse SHT: grid rows -> fft/L -> phase -> weighted fold -> node halves
 template <bool SM>
-__global__ void __launch_bounds__(kDftThreads, SM ? 1 : 2) sht_anal_kernel(
+__global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, double *__restrict__ arena,
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
