@@ -170,23 +170,49 @@ __device__ void generic_pass(double2 *buf, int nrows, int L, int span, int P, co
     for (int g0 = 0; g0 < total; g0 += NB) {
         __syncthreads();   // roots written / previous batch's staging consumed
         // staging, item = j * NB + bi: consecutive threads take consecutive
-        // butterflies (consecutive k), so the loads coalesce when span > 1
-        for (int it = threadIdx.x; it < NB * W; it += blockDim.x) {
-            const int j = it / NB, bi = it - j * NB, gi = g0 + bi;
-            if (gi >= total) continue;
-            const int rw = gi >= nb ? gi / nb : 0, tt = gi - rw * nb;
-            const int gg = tt / span, k = tt - gg * span;
-            const double2 *row = buf + (int64_t)rw * L + gg * span * P + k;
-            double2 xj = row[j * span];
-            if (j > 0 && span > 1) xj = cmul(xj, conjif(Tw[(j - 1) * span + k], inv));
-            if (j == 0) {
-                s_a[bi] = xj;
-                s_b[bi] = make_double2(0.0, 0.0);
-            } else {
-                double2 xm = row[(P - j) * span];
-                if (span > 1) xm = cmul(xm, conjif(Tw[(P - j - 1) * span + k], inv));
-                s_a[j * NB + bi] = make_double2(xj.x + xm.x, xj.y + xm.y);
-                s_b[j * NB + bi] = make_double2(xj.x - xm.x, xj.y - xm.y);
+        // butterflies (consecutive k), so the loads coalesce when span > 1;
+        // kGenU items per thread have all their loads in flight before any
+        // is used (rows in global scratch: the loads are L2 round trips)
+        constexpr int kGenU = 4;
+        for (int it0 = threadIdx.x; it0 < NB * W; it0 += kGenU * blockDim.x) {
+            double2 xj[kGenU], xm[kGenU], tj[kGenU], tm[kGenU];
+            int jj[kGenU], bb[kGenU];
+#pragma unroll
+            for (int u = 0; u < kGenU; ++u) {
+                const int it = it0 + u * blockDim.x;
+                const int j = it / NB, bi = it - j * NB, gi = g0 + bi;
+                jj[u] = (it < NB * W && gi < total) ? j : -1;
+                bb[u] = bi;
+                xj[u] = xm[u] = tj[u] = tm[u] = make_double2(0.0, 0.0);
+                if (jj[u] < 0) continue;
+                const int rw = gi >= nb ? gi / nb : 0, tt = gi - rw * nb;
+                const int gg = tt / span, k = tt - gg * span;
+                const double2 *row = buf + (int64_t)rw * L + gg * span * P + k;
+                xj[u] = row[j * span];
+                if (j > 0) {
+                    xm[u] = row[(P - j) * span];
+                    if (span > 1) {
+                        tj[u] = Tw[(j - 1) * span + k];
+                        tm[u] = Tw[(P - j - 1) * span + k];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kGenU; ++u) {
+                const int j = jj[u], bi = bb[u];
+                if (j < 0) continue;
+                if (j == 0) {
+                    s_a[bi] = xj[u];
+                    s_b[bi] = make_double2(0.0, 0.0);
+                } else {
+                    double2 a = xj[u], c = xm[u];
+                    if (span > 1) {
+                        a = cmul(a, conjif(tj[u], inv));
+                        c = cmul(c, conjif(tm[u], inv));
+                    }
+                    s_a[j * NB + bi] = make_double2(a.x + c.x, a.y + c.y);
+                    s_b[j * NB + bi] = make_double2(a.x - c.x, a.y - c.y);
+                }
             }
         }
         __syncthreads();
@@ -428,9 +454,25 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     dft_passes(buf, 2, d, Wt, W + L, true);
     double2 *up = grid + (int64_t)(r_count + rr) * L;
     double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
-    for (int j = threadIdx.x; j < L; j += blockDim.x) {
-        up[j] = buf[j];
-        lo[j] = buf[L + j];
+    // batched so several (scratch-path: L2) loads are in flight per thread
+    for (int j0 = threadIdx.x; j0 < L; j0 += 4 * blockDim.x) {
+        double2 vu[4], vl[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < L) {
+                vu[u] = buf[j];
+                vl[u] = buf[L + j];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < L) {
+                up[j] = vu[u];
+                lo[j] = vl[u];
+            }
+        }
     }
     __syncthreads();
     }
