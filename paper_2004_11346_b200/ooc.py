@@ -136,7 +136,6 @@ class ChunkedSht:
             self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, 0,
             _ptr(self.ybuf), self._stream()), "bfsht_synth_rows")
         self.resident = {}
-        self.times = {}
 
     # ------------------------------------------------------------ helpers
     def _stream(self):
@@ -325,8 +324,8 @@ class ChunkedSht:
         rep["copy_ms"] = t.get("copy", 0.0)
         rep["device_ms"] = alt + rep["dft_ms"] + rep["pack_ms"] + rep["copy_ms"]
         rep["alt_gbs"] = rep["alt_bytes"] / (alt * 1e-3) / 1e9 if alt > 0 else 0.0
-        per = sorted((k, v) for k, v in t.items() if k.startswith("alt"))
-        rep["alt_ms_per_chunk"] = [round(v, 3) for _, v in per]
+        per = sorted((int(k[3:]), v) for k, v in t.items() if k.startswith("alt"))
+        rep["alt_ms_per_chunk"] = [round(v, 3) for _, v in per]   # by chunk index
 
     def node_entries(self, m):
         """Host copy of order m's node-half entries in the θ-major buffer:
