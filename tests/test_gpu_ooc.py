@@ -75,3 +75,32 @@ def test_dft_rows_large_prime_radices(L):
     xt = torch.from_numpy(x).cuda()
     assert rel(dft_rows(xt).cpu().numpy(), np.fft.fft(x, axis=1)) < 1e-14
     assert rel(dft_rows(xt, inverse=True).cpu().numpy(), L * np.fft.ifft(x, axis=1)) < 1e-14
+
+
+def test_chunked_sht_subset_of_chunks():
+    # a chunk subset (the sampled N=8192 run's mode): coefficients on those
+    # orders only; the full-size DFT stage sees zeros elsewhere
+    import torch
+    from paper_2004_11346_b200 import plan_orders
+    from paper_2004_11346_b200.ooc import ChunkedSht
+
+    n = 16
+    run = ChunkedSht(n, 4, n0=16, processes=1, only=[2])
+    plans = plan_orders(n, range(2 * n), n0=16, processes=1)
+    sub = set(run.chunks[2])
+    flat = random_flat(n, 3)
+    _, offs = OA.coeff_offsets(n)
+    for i, m in enumerate(range(-(2 * n - 1), 2 * n)):
+        if abs(m) not in sub:
+            flat[offs[i]:offs[i + 1]] = 0.0
+    grid = torch.empty((2 * n, 4 * n - 1), dtype=torch.complex128, device="cuda")
+    run.forward(flat, grid)
+    got = grid.cpu().numpy()
+    want = OA.sht_forward(plans, n, flat)
+    assert rel(got, want) < 1e-12
+    back = run.inverse(grid)["coeffs"]
+    want_b = OA.sht_inverse(plans, n, got)
+    sel = np.concatenate([np.arange(offs[i], offs[i + 1])
+                          for i, m in enumerate(range(-(2 * n - 1), 2 * n)) if abs(m) in sub])
+    assert rel(back[sel], want_b[sel]) < 1e-12
+    run.close()
