@@ -69,7 +69,8 @@ typedef struct {
     /* On-GPU regeneration of dense turning tiles.  A
      * fraction regen in [0, 1] of the full-height (32-row) tiles of kind-2
      * blocks is stored as recurrence seeds (per row: p_prev, p_cur, 2^e at
-     * the tile's first degree) instead of values; the engine re-runs the
+     * the tile's first degree, and at column 16 for tiles wider than 16;
+     * format.h bf_seed_doubles) instead of values; the engine re-runs the
      * reference recurrence (kernels/_recur_cy.pyx:18-67) bit for bit.
      * Needs the nodes and start values below; regen = 0 ignores them. */
     double regen;
@@ -106,9 +107,11 @@ int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]);
 /* alpha_s, beta_s (s = 0 .. k_max-m-1) of the degree recurrence
  * (kernels/common.py:37-53), interleaved; for tests of the seed path. */
 int bfsht_rec_coeffs(int64_t m, int64_t k_max, double *out);
-/* Regenerate one seeded tile on the host exactly as the engine does (test
- * oracle of the device generation): seed block at `seed`, R x C tile in
- * the 4x4-block layout into out (bf_tile_doubles(R, C) doubles). */
+/* Regenerate one seeded tile on the host with the reference step sequence
+ * (range test after every step), chain by chain from the seed block's
+ * states — the test oracle of the device generation: seed block at `seed`,
+ * R x C tile in the 4x4-block layout into out (bf_tile_doubles(R, C)
+ * doubles). */
 int bfsht_regen_tile_host(const double *seed, int R, int C, const double *rec,
                           const double *x_pos, double mag_min, double *out);
 void bfsht_packed_free(bfsht_packed *p);
