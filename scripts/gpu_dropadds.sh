@@ -1,3 +1,5 @@
+# Timing-only experiment (round 1): BFSHT_DEBUG_DROP_ADDS was a temporary packer patch
+# (drop every index-add op; wrong results) that is not in the tree any more.
 mkdir -p gpurun_out
 python -m paper_2004_11346_b200.build > gpurun_out/build.log 2>&1
 timeout 600 python scripts/stage_times.py --reps 5 > gpurun_out/st_base.jsonl 2>/dev/null
