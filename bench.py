@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=1,
                     help="C2 with B <= 4 independent transforms per step sharing one "
                          "payload pass (16-RHS engine); default 1 = the single transform")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="run the multi-GPU (order-sharded, NCCL) runner even at one "
+                         "rank: exercises the scaling path of this script on one GPU")
     ap.add_argument("--regen", type=float, default=0.0,
                     help="fraction of full-height dense turning tiles regenerated "
                          "on the GPU from recurrence seeds (SURVEY f1)")
@@ -302,15 +305,22 @@ def run_ours(args):
     if world > 1 and args.batch > 1:
         raise SystemExit("--batch > 1 is single-GPU only")
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.force_sharded
+    if sharded and args.batch > 1:
+        raise SystemExit("--batch > 1 is single-GPU only")
+    if sharded:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if world == 1:
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = args.n
     params = SamplingConfig(tolerance=args.tol)
     procs = args.plan_procs or max(1, (os.cpu_count() or 1) // world)
 
     t0 = time.time()
-    if world == 1:
+    if not sharded:
         orders = list(range(2 * n))
     else:
         orders = D.lpt_orders(n, world)[rank]
@@ -319,7 +329,7 @@ def run_ours(args):
     payload_values = sum(p.stats["total_nnz"] for p in plans)
 
     t0 = time.time()
-    if world == 1:
+    if not sharded:
         eng = ShtDevice.__new__(ShtDevice)
         eng.n = n
         eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights, regen=args.regen)
@@ -409,7 +419,7 @@ def run_ours(args):
         e2e["ms"] = float(t.item())
     # the host output of the last timed step must be the input back
     want = torch.from_numpy(np.ascontiguousarray(
-        runner.shard_coeffs(flat) if world > 1 else runner.host_coeffs(flat)))
+        runner.shard_coeffs(flat) if sharded else runner.host_coeffs(flat)))
     got = runner.last_e2e_output
     t = torch.tensor([float(torch.linalg.norm(got - want)) ** 2,
                       float(torch.linalg.norm(want)) ** 2], device=dev, dtype=torch.float64)
@@ -418,7 +428,7 @@ def run_ours(args):
     e2e_rt = float((t[0] / t[1]).sqrt())
 
     check = None
-    if args.check and world == 1:
+    if args.check and not sharded:
         import oracle.apply as OA
         g = (grid[0] if args.batch > 1 else grid).cpu().numpy()
         want = OA.sht_forward(plans, n, flat)
@@ -463,7 +473,7 @@ def run_ours(args):
         if check is not None:
             line["check_rel_l2_vs_oracle"] = check
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         torch.distributed.destroy_process_group()
     return 0
 
