@@ -95,14 +95,13 @@ int bfsht_pack_plan(const bfsht_manifest *man, int threads,
  * (dependency-free dense) stage of the forward/inverse direction,
  * 18 regenerated tiles, 19 reference values they replace (not stored),
  * 20 doubles of the recurrence-coefficient table, 21 doubles of x_pos,
- * 22 bit pattern of mag_min (double), 23 length of the dataflow order
- * (0 when the plan only supports staged launches) */
+ * 22 bit pattern of mag_min (double); 16, 17 and 23 are reserved (-1, -1,
+ * 0) */
 #define BFSHT_INFO_LEN 24
 int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_LEN]);
 /* arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves, 6/7 stage
  * bounds fwd/inv, 8 recurrence coefficients (alpha, beta pairs), 9 x_pos,
- * 10 dataflow claim order (task ids, forward direction then inverse),
- * 11 per-task int32: stage | (dependency stage + 1) << 8 */
+ * 10, 11 reserved (NULL) */
 int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]);
 /* alpha_s, beta_s (s = 0 .. k_max-m-1) of the degree recurrence
  * (kernels/common.py:37-53), interleaved; for tests of the seed path. */
@@ -122,28 +121,18 @@ const char *bfsht_last_error(void);
 typedef struct bfsht_plan bfsht_plan;       /* opaque device plan */
 
 /* Upload a packed plan (arrays as returned by bfsht_packed_arrays) to the
- * current device. */
+ * current device.  A plan remembers its device: every call below that takes
+ * a plan runs on that device and restores the caller's current device. */
 int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out);
 /* Device arrays already resident (e.g. allocated through torch), borrowed:
  * dev[0..5] = tiles, ops, idx, maps, tasks, halves (bfsht_packed_arrays
  * order), dev[6] = vector arena (info[5] x 4 doubles), dev[7] = recurrence
  * coefficients, dev[8] = x_pos (both only read by regenerated tiles, may
- * be NULL when info[18] == 0), dev[9] = dataflow order, dev[10] = task
- * stage/dependency words (both NULL: staged launches only); host[5..7] =
+ * be NULL when info[18] == 0), dev[9..11] reserved (NULL); host[5..7] =
  * host copies of halves and the two stage-bound arrays. */
 int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
                     void *const dev[12], bfsht_plan **out);
 void bfsht_plan_free(bfsht_plan *pl);
-/* Scheduling knobs: overlap = run the dependency-free dense stage on its
- * own SMs concurrently with the butterfly/low-rank chain (default 1, only
- * for plans packed with BFSHT_SPLIT_FREE=1); chain_ctas = SMs given to the
- * chain (0 = default 27%). */
-int bfsht_plan_tune(bfsht_plan *pl, int overlap, int chain_ctas);
-/* Schedule of bfsht_alt_apply: 1 = dataflow (one persistent launch per
- * direction, tasks claimed in the packer's dataflow order, each waiting only
- * for the stage it reads), 0 = one launch per stage (default: 1-2% faster
- * at N=1024 on B200).  Results are bitwise identical either way. */
-int bfsht_plan_schedule(bfsht_plan *pl, int dataflow);
 /* Device pointer to the vector arena (info[5] entries x 4 doubles). */
 double *bfsht_plan_arena(bfsht_plan *pl);
 

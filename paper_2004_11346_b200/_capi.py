@@ -43,10 +43,6 @@ def declare(lib):
     lib.bfsht_sht_inverse.argtypes = [_P, _P, _P, _P, _P]
     lib.bfsht_dft_rows.restype = _I
     lib.bfsht_dft_rows.argtypes = [_I64, _I64, _I, _P, _P, _P]
-    lib.bfsht_plan_schedule.restype = _I
-    lib.bfsht_plan_schedule.argtypes = [_P, _I]
-    lib.bfsht_plan_tune.restype = _I
-    lib.bfsht_plan_tune.argtypes = [_P, _I, _I]
     lib.bfsht_reset_launches.restype = _I
     lib.bfsht_reset_launches.argtypes = [_P]
     for name in ("bfsht_shard_pack", "bfsht_shard_unpack"):
@@ -65,8 +61,7 @@ def declare(lib):
 EXPORTS = (
     "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
     "bfsht_packed_free", "bfsht_rec_coeffs", "bfsht_regen_tile_host", "bfsht_last_error", "bfsht_plan_upload",
-    "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena", "bfsht_plan_tune",
-    "bfsht_plan_schedule",
+    "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
     "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_alt_fields",
     "bfsht_half_apply", "bfsht_sht_batch", "bfsht_alt_apply_wide",
     "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",

@@ -58,8 +58,10 @@ def _torch():
     return torch
 
 
-def _stream_ptr(torch, stream=None):
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream_ptr(torch, stream=None, device=None):
+    """The given stream, else the current stream OF THE PLAN'S DEVICE (the
+    C ABI switches to the plan's device for the call)."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
 
 
@@ -96,8 +98,6 @@ class DevicePlan:
                 up(pk.halves.view(np.int32)),
                 up(pk.rec if pk.rec.size else np.zeros(2)),
                 up(pk.xpos if pk.xpos.size else np.zeros(2)),
-                up(pk.flow if pk.flow.size else np.zeros(1, np.int32)),
-                up(pk.tinfo if pk.tinfo.size else np.zeros(1, np.int32)),
             ]
             self.arena = torch.zeros((max(pk.stats["arena"], 1), NRHS),
                                      dtype=torch.float64, device=self.device)
@@ -120,9 +120,6 @@ class DevicePlan:
             dev[6] = self.arena.data_ptr()
             dev[7] = self._dev[6].data_ptr()
             dev[8] = self._dev[7].data_ptr()
-            if pk.flow.size:
-                dev[9] = self._dev[8].data_ptr()
-                dev[10] = self._dev[9].data_ptr()
             h = ctypes.c_void_p()
             check(self.lib, self.lib.bfsht_plan_wrap(info, host, dev,
                                                      ctypes.byref(h)),
@@ -141,25 +138,19 @@ class DevicePlan:
     def launches(self):
         return int(self.lib.bfsht_plan_launches(self.handle))
 
-    def set_schedule(self, dataflow=True):
-        """ALT schedule: dataflow (one persistent launch per direction) or
-        one launch per stage (the default); results are bitwise identical."""
-        check(self.lib, self.lib.bfsht_plan_schedule(self.handle, 1 if dataflow else 0),
-              "bfsht_plan_schedule")
-
     # -------------------------------------------------------------- apply
     def alt_apply(self, direction, stream=None):
         """All ALT stages over the arena (inputs already in place)."""
         torch = _torch()
         check(self.lib, self.lib.bfsht_alt_apply(
-            self.handle, direction, _stream_ptr(torch, stream)), "bfsht_alt_apply")
+            self.handle, direction, _stream_ptr(torch, stream, self.device)), "bfsht_alt_apply")
 
     def alt_apply_wide(self, direction, stream=None):
         """All ALT stages over the wide (16-RHS) arena, inputs in place."""
         torch = _torch()
         check(self.lib, self.lib.bfsht_alt_apply_wide(
             self.handle, direction, ctypes.c_void_p(self.wide_arena().data_ptr()),
-            _stream_ptr(torch, stream)), "bfsht_alt_apply_wide")
+            _stream_ptr(torch, stream, self.device)), "bfsht_alt_apply_wide")
 
     def alt_orders(self, direction, inp, out=None, stream=None):
         """Per-order ALT on device complex128 tensors laid out plan after
@@ -175,7 +166,7 @@ class DevicePlan:
         check(self.lib, self.lib.bfsht_alt_orders(
             self.handle, direction, ctypes.c_void_p(inp.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
-            _stream_ptr(torch, stream)), "bfsht_alt_orders")
+            _stream_ptr(torch, stream, self.device)), "bfsht_alt_orders")
         return out
 
     def wide_arena(self):
@@ -204,7 +195,7 @@ class DevicePlan:
             self.handle, direction, nf, ctypes.c_void_p(inp.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
             ctypes.c_void_p(self.wide_arena().data_ptr()),
-            _stream_ptr(torch, stream)), "bfsht_alt_fields")
+            _stream_ptr(torch, stream, self.device)), "bfsht_alt_fields")
         return out
 
     def sht_batch(self, direction, inp, out=None, stream=None):
@@ -223,7 +214,7 @@ class DevicePlan:
             self.handle, direction, int(nb), ctypes.c_void_p(inp.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
             ctypes.c_void_p(self.wide_arena().data_ptr()),
-            _stream_ptr(torch, stream)), "bfsht_sht_batch")
+            _stream_ptr(torch, stream, self.device)), "bfsht_sht_batch")
         return out
 
     def half_apply(self, direction, half, x, stream=None):
@@ -238,7 +229,7 @@ class DevicePlan:
             self.handle, direction, int(half), int(x.shape[1]),
             ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
             ctypes.c_void_p(self.wide_arena().data_ptr()),
-            _stream_ptr(torch, stream)), "bfsht_half_apply")
+            _stream_ptr(torch, stream, self.device)), "bfsht_half_apply")
         return out
 
     def sht_forward(self, coeffs, out=None, stream=None):
@@ -249,7 +240,7 @@ class DevicePlan:
                               device=self.device)
         check(self.lib, self.lib.bfsht_sht_forward(
             self.handle, ctypes.c_void_p(coeffs.data_ptr()),
-            ctypes.c_void_p(out.data_ptr()), _stream_ptr(torch, stream)),
+            ctypes.c_void_p(out.data_ptr()), _stream_ptr(torch, stream, self.device)),
             "bfsht_sht_forward")
         return out
 
@@ -262,7 +253,7 @@ class DevicePlan:
             self.handle, ctypes.c_void_p(grid.data_ptr()),
             ctypes.c_void_p(out.data_ptr()),
             ctypes.c_void_p(self.weights.data_ptr()),
-            _stream_ptr(torch, stream)), "bfsht_sht_inverse")
+            _stream_ptr(torch, stream, self.device)), "bfsht_sht_inverse")
         return out
 
     def close(self):
@@ -624,8 +615,9 @@ def dft_rows(x, inverse=False, stream=None):
     x = x.contiguous()
     out = torch.empty_like(x)
     rows, L = x.shape
-    check(lib, lib.bfsht_dft_rows(L, rows, INVERSE if inverse else FORWARD,
-                                  ctypes.c_void_p(x.data_ptr()),
-                                  ctypes.c_void_p(out.data_ptr()),
-                                  _stream_ptr(torch, stream)), "bfsht_dft_rows")
+    with torch.cuda.device(x.device):
+        check(lib, lib.bfsht_dft_rows(L, rows, INVERSE if inverse else FORWARD,
+                                      ctypes.c_void_p(x.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr()),
+                                      _stream_ptr(torch, stream, x.device)), "bfsht_dft_rows")
     return out

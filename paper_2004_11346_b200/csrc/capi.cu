@@ -5,7 +5,10 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "bfsht_b200.h"
@@ -14,6 +17,20 @@
 static thread_local std::string g_err;
 
 void bfsht_set_error(const std::string &msg) { g_err = msg; }
+
+int bf_ensure_smem(const void *func, int bytes) {
+    if (bytes <= 48 * 1024) return 0;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, int> high;
+    int dev = 0;
+    BF_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    int &h = high[{dev, func}];
+    if (bytes <= h) return 0;
+    BF_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    h = bytes;
+    return 0;
+}
 
 int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStream_t st);
 int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const double *weights,
@@ -70,28 +87,12 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
                                cudaMemcpyHostToDevice));
         }
     }
-    if (pl->flow && pl->tinfo && pl->info[23] > 0) {
-        const size_t nc = 2 * (BFSHT_MAX_FLOW_STAGES + 1);
-        BF_CUDA(cudaMalloc(&pl->flow_ctr, sizeof(int) * nc));
-        pl->owned.push_back(pl->flow_ctr);
-        BF_CUDA(cudaMemset(pl->flow_ctr, 0, sizeof(int) * nc));
-        std::vector<int> need(2 * BFSHT_MAX_FLOW_STAGES, 0);
-        for (int d = 0; d < 2; ++d)
-            for (size_t s = 0; s + 1 < pl->stages[d].size() && s < BFSHT_MAX_FLOW_STAGES; ++s)
-                need[d * BFSHT_MAX_FLOW_STAGES + s] = (int)(pl->stages[d][s + 1] - pl->stages[d][s]);
-        BF_CUDA(cudaMalloc(&pl->flow_need, sizeof(int) * need.size()));
-        pl->owned.push_back(pl->flow_need);
-        BF_CUDA(cudaMemcpy(pl->flow_need, need.data(), sizeof(int) * need.size(),
-                           cudaMemcpyHostToDevice));
-    } else {
-        pl->flow = nullptr;
-        pl->tinfo = nullptr;
-    }
     pl->ncounters = (int)std::max(pl->info[7], pl->info[8]) + 1;
     BF_CUDA(cudaMalloc(&pl->counters, sizeof(int) * pl->ncounters));
     pl->owned.push_back(pl->counters);
     int dev = 0;
     BF_CUDA(cudaGetDevice(&dev));
+    pl->device = dev;
     BF_CUDA(cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev));
     return 0;
 }
@@ -115,17 +116,15 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     }
     const void *arr[12];
     bfsht_packed_arrays(p, arr);
-    // device copies of arrays 0..5 and 8..11 (stage bounds stay on the host)
-    const int which[10] = {0, 1, 2, 3, 4, 5, 8, 9, 10, 11};
-    const size_t sz[10] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
-                           (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
-                           (size_t)pl->info[4] * sizeof(bf_task),
-                           (size_t)pl->info[6] * sizeof(bf_half),
-                           (size_t)pl->info[20] * 8, (size_t)pl->info[21] * 8,
-                           (size_t)pl->info[23] * 4,
-                           (size_t)(pl->info[23] > 0 ? pl->info[4] : 0) * 4};
-    void *dev[10];
-    for (int i = 0; i < 10; ++i) {
+    // device copies of arrays 0..5 and 8..9 (stage bounds stay on the host)
+    const int which[8] = {0, 1, 2, 3, 4, 5, 8, 9};
+    const size_t sz[8] = {(size_t)pl->info[0] * 8, (size_t)pl->info[1] * sizeof(bf_op),
+                          (size_t)pl->info[2] * 4, (size_t)pl->info[3] * BF_SLOTS,
+                          (size_t)pl->info[4] * sizeof(bf_task),
+                          (size_t)pl->info[6] * sizeof(bf_half),
+                          (size_t)pl->info[20] * 8, (size_t)pl->info[21] * 8};
+    void *dev[8];
+    for (int i = 0; i < 8; ++i) {
         dev[i] = nullptr;
         if (cudaMalloc(&dev[i], sz[i] ? sz[i] : 16) != cudaSuccess ||
             (sz[i] && cudaMemcpy(dev[i], arr[which[i]], sz[i], cudaMemcpyHostToDevice) != cudaSuccess)) {
@@ -157,8 +156,6 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     pl->halves = (const bf_half *)dev[5];
     pl->rec = (const double *)dev[6];
     pl->xpos = (const double *)dev[7];
-    pl->flow = (const int32_t *)dev[8];
-    pl->tinfo = (const int32_t *)dev[9];
     pl->arena = (double *)arena;
     int rc = finish_plan(pl, (const bf_half *)arr[5], (const int64_t *)arr[6],
                          (const int64_t *)arr[7]);
@@ -187,8 +184,6 @@ int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8
     pl->arena = (double *)dev[6];
     pl->rec = (const double *)dev[7];
     pl->xpos = (const double *)dev[8];
-    pl->flow = (const int32_t *)dev[9];
-    pl->tinfo = (const int32_t *)dev[10];
     if (info[18] > 0 && (!pl->rec || !pl->xpos)) {
         delete pl;
         g_err = "plan has regenerated tiles but no coefficient table / nodes";
@@ -206,34 +201,23 @@ int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8
 
 void bfsht_plan_free(bfsht_plan *pl) {
     if (!pl) return;
-    if (pl->side) cudaStreamDestroy(pl->side);
-    if (pl->ev_fork) cudaEventDestroy(pl->ev_fork);
-    if (pl->ev_join) cudaEventDestroy(pl->ev_join);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != pl->device) cudaSetDevice(pl->device);
     for (void *p : pl->owned) cudaFree(p);
     for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
                     (void *)pl->dft_scratch})
         if (p) cudaFree(p);
+    if (cur != pl->device) cudaSetDevice(cur);
     delete pl;
 }
 
 double *bfsht_plan_arena(bfsht_plan *pl) { return pl ? pl->arena : nullptr; }
 
-int bfsht_plan_schedule(bfsht_plan *pl, int dataflow) {
-    if (!pl) return -1;
-    pl->dataflow = dataflow != 0;
-    return 0;
-}
-
-int bfsht_plan_tune(bfsht_plan *pl, int overlap, int chain_ctas) {
-    if (!pl) return -1;
-    pl->overlap = overlap != 0;
-    pl->chain_ctas = chain_ctas;
-    return 0;
-}
-
 int64_t bfsht_plan_launches(bfsht_plan *pl) { return pl ? pl->launches : -1; }
 
 int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan or direction";
         return -1;
@@ -243,6 +227,7 @@ int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream) {
 }
 
 int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan or direction";
         return -1;
@@ -258,6 +243,7 @@ int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
 
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
                      const double *weights, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan or direction";
         return -1;
@@ -272,6 +258,7 @@ int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
 
 int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, double *out,
                      const double *weights, double *work, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan or direction";
         return -1;
@@ -289,6 +276,7 @@ int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, dou
 
 int bfsht_half_apply(bfsht_plan *pl, int dir, int half, int k, const double *in, double *out,
                      double *work, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan or direction";
         return -1;
@@ -323,6 +311,7 @@ static int check_sht(bfsht_plan *pl) {
 }
 
 int bfsht_alt_apply_wide(bfsht_plan *pl, int dir, double *work, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl || !work || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad plan, direction or work arena";
         return -1;
@@ -332,6 +321,7 @@ int bfsht_alt_apply_wide(bfsht_plan *pl, int dir, double *work, void *stream) {
 
 int bfsht_sht_batch(bfsht_plan *pl, int dir, int batch, const double *in, double *out,
                     const double *weights, double *work, void *stream) {
+    DeviceGuard guard(pl);
     int rc = check_sht(pl);
     if (rc) return rc;
     if (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE) {
@@ -350,6 +340,7 @@ int bfsht_sht_batch(bfsht_plan *pl, int dir, int batch, const double *in, double
 }
 
 int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, void *stream) {
+    DeviceGuard guard(pl);
     if (check_sht(pl)) return -1;
 
     return bf_sht_forward(pl, coeffs, grid, (cudaStream_t)stream);
@@ -357,6 +348,7 @@ int bfsht_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, void *
 
 int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
                       const double *weights, void *stream) {
+    DeviceGuard guard(pl);
     if (check_sht(pl)) return -1;
     if (!weights) {
         g_err = "inverse SHT needs quadrature weights";
@@ -368,18 +360,29 @@ int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
 
 int bfsht_dft_rows(int64_t L, int64_t rows, int dir, const double *in, double *out,
                    void *stream) {
-    static thread_local bfsht_plan *scratch_plan = nullptr;
     if (L < 1 || rows < 0 || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
         g_err = "bad DFT arguments";
         return -1;
     }
-    if (!scratch_plan) {
-        scratch_plan = new bfsht_plan();
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&scratch_plan->sm_count, cudaDevAttrMultiProcessorCount, dev);
+    // DFT tables live in a per-(thread, device) context plan that keeps the
+    // tables of the last length used (re-prepared, old tables freed, when
+    // the length changes); it is freed with the thread
+    struct Ctx {
+        std::map<int, bfsht_plan *> by_dev;
+        ~Ctx() {
+            for (auto &kv : by_dev) bfsht_plan_free(kv.second);
+        }
+    };
+    static thread_local Ctx ctx;
+    int dev = 0;
+    BF_CUDA(cudaGetDevice(&dev));
+    bfsht_plan *&pl = ctx.by_dev[dev];
+    if (!pl) {
+        pl = new bfsht_plan();
+        pl->device = dev;
+        BF_CUDA(cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev));
     }
-    return bf_dft_rows(scratch_plan, L, rows, dir, in, out, (cudaStream_t)stream);
+    return bf_dft_rows(pl, L, rows, dir, in, out, (cudaStream_t)stream);
 }
 
 }  // extern "C"

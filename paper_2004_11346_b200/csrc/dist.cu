@@ -85,6 +85,7 @@ int grid_for(int64_t count) {
 extern "C" {
 
 int bfsht_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     if (pl->norders == 0) return 0;
     dim3 g((pl->n + 255) / 256, pl->norders);
@@ -96,6 +97,7 @@ int bfsht_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs, v
 }
 
 int bfsht_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     if (pl->norders == 0) return 0;
     dim3 g((pl->n + 255) / 256, pl->norders);
@@ -108,6 +110,7 @@ int bfsht_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs, void 
 
 int bfsht_gather_entries(bfsht_plan *pl, const int32_t *idx, int64_t count, double *out,
                          void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     if (count <= 0) return 0;
     gather_entries_kernel<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(
@@ -120,6 +123,7 @@ int bfsht_gather_entries(bfsht_plan *pl, const int32_t *idx, int64_t count, doub
 
 int bfsht_scatter_entries(bfsht_plan *pl, const int32_t *idx, int64_t count, const double *in,
                           void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     if (count <= 0) return 0;
     scatter_entries_kernel<<<grid_for(count), 256, 0, (cudaStream_t)stream>>>(
@@ -132,6 +136,7 @@ int bfsht_scatter_entries(bfsht_plan *pl, const int32_t *idx, int64_t count, con
 
 int bfsht_synth_rows(bfsht_plan *pl, const void *halves, const double *ybuf, int64_t r_begin,
                      int64_t r_count, double *grid, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     return bf_synth_rows(pl, (const bf_half *)halves, ybuf, (int)r_begin, (int)r_count, grid,
                          (cudaStream_t)stream);
@@ -139,12 +144,14 @@ int bfsht_synth_rows(bfsht_plan *pl, const void *halves, const double *ybuf, int
 
 int bfsht_anal_rows(bfsht_plan *pl, const void *halves, double *ubuf, int64_t r_begin,
                     int64_t r_count, const double *grid, const double *weights, void *stream) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     return bf_anal_rows(pl, (const bf_half *)halves, ubuf, (int)r_begin, (int)r_count, grid,
                         weights, (cudaStream_t)stream);
 }
 
 int bfsht_reset_launches(bfsht_plan *pl) {
+    DeviceGuard guard(pl);
     if (!pl) return -1;
     pl->launches = 0;
     return 0;

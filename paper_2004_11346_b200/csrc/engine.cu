@@ -143,13 +143,6 @@ struct StageArgs {
     const double *rec;     // recurrence coefficients (regenerated tiles)
     const double *xpos;    // positive nodes
     double mag_min;
-    // dataflow schedule (flow != nullptr): claim index t runs task flow[t];
-    // tinfo[task] = stage | (dependency stage + 1) << 8; done[s] counts
-    // finished tasks of stage s, need[s] its task count
-    const int32_t *flow;
-    const int32_t *tinfo;
-    int *done;
-    const int *need;
 };
 
 __device__ __forceinline__ bf_op load_op(const bf_op *p) {
@@ -167,8 +160,6 @@ __device__ __forceinline__ bf_op load_op(const bf_op *p) {
 struct Rec {
     bf_op op;
     int out, nout, last, valid;
-    int dep;      // dataflow: stage this op must wait for (-1: none)
-    int stage;    // dataflow: stage of the op's task
 };
 
 // Walks the global task list as one flat op stream, one op per call.  Tasks
@@ -177,10 +168,8 @@ struct Rec {
 // loaded, so neither the atomic nor the record load stalls the warp.
 struct Cursor {
     int base, n, i, out, nout;   // current task
-    int stage, dep;              // its dataflow stage / dependency
     int nt;                      // next task id (uniform)
     bf_task ntask;               // its record (valid when nt < ntasks)
-    int ninfo;                   // its dataflow word
     int raw;                     // lane 0: claimed id of the task after next
 };
 
@@ -190,41 +179,14 @@ __device__ __forceinline__ int claim_raw(const StageArgs &a, int lane) {
 
 __device__ __forceinline__ int bcast(int raw) { return __shfl_sync(0xffffffffu, raw, 0); }
 
-__device__ __forceinline__ bf_task load_task(const StageArgs &a, int t, int &info) {
-    const int64_t id = a.flow ? (int64_t)__ldg(a.flow + t) : a.t0 + t;
-    const int4 v = __ldg(reinterpret_cast<const int4 *>(a.tasks + id));
-    info = a.flow ? __ldg(a.tinfo + id) : 0;
+__device__ __forceinline__ bf_task load_task(const StageArgs &a, int t) {
+    const int4 v = __ldg(reinterpret_cast<const int4 *>(a.tasks + a.t0 + t));
     bf_task k;
     k.op_begin = v.x;
     k.op_count = v.y;
     k.out = v.z;
     k.nout = v.w;
     return k;
-}
-
-// dataflow: has stage `dep` finished?  (lane 0 polls with acquire; the
-// async-proxy fence orders the bulk copies that read its outputs)
-__device__ __forceinline__ bool stage_done(const StageArgs &a, int dep, int lane) {
-    int ok = 0;
-    if (lane == 0) {
-        int v;
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.done + dep) : "memory");
-        ok = v >= __ldg(a.need + dep);
-    }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (ok) asm volatile("fence.proxy.async.global;" ::: "memory");
-    return ok != 0;
-}
-
-// dataflow: block until stage `dep` has finished.  Only called with an
-// empty ring (every task this warp started is finished and counted), and a
-// task's dependency precedes it in the claim order, so the wait always ends;
-// a bound turns a broken schedule into a trap instead of a hung GPU.
-__device__ __noinline__ void wait_stage(const StageArgs &a, int dep, int lane) {
-    for (long long it = 0; !stage_done(a, dep, lane); ++it) {
-        __nanosleep(200);
-        if (it > (1LL << 25)) __trap();
-    }
 }
 
 __device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) {
@@ -236,12 +198,10 @@ __device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) 
         c.n = c.ntask.op_count;
         c.out = c.ntask.out;
         c.nout = c.ntask.nout;
-        c.stage = c.ninfo & 0xff;
-        c.dep = (c.ninfo >> 8) - 1;
         c.i = 0;
         c.nt = bcast(c.raw);
         if (c.nt < a.ntasks) {
-            c.ntask = load_task(a, c.nt, c.ninfo);
+            c.ntask = load_task(a, c.nt);
             c.raw = claim_raw(a, lane);
         }
     }
@@ -250,8 +210,6 @@ __device__ __forceinline__ Rec advance(const StageArgs &a, Cursor &c, int lane) 
     r.nout = c.nout;
     r.last = (c.i == c.n - 1);
     r.valid = 1;
-    r.dep = c.i == 0 ? c.dep : -1;
-    r.stage = c.stage;
     ++c.i;
     return r;
 }
@@ -440,7 +398,7 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing<NR> &ring, in
     const bool gather = (op.flags & BF_OPF_GATHER) != 0;
     if (lane == 0) {
         ring.meta[s] = op;
-        ring.tmeta[s] = make_int4(r.out, r.nout, r.last, r.stage);
+        ring.tmeta[s] = make_int4(r.out, r.nout, r.last, 0);
     }
     uint32_t bytes = 0;
     int nvec = 0;
@@ -631,13 +589,10 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
     Cursor cur;
     cur.n = cur.i = 0;
     cur.base = cur.out = cur.nout = 0;
-    cur.stage = 0;
-    cur.dep = -1;
-    cur.ninfo = 0;
     cur.nt = bcast(claim_raw(a, lane));
     cur.raw = 0;
     if (cur.nt < a.ntasks) {
-        cur.ntask = load_task(a, cur.nt, cur.ninfo);
+        cur.ntask = load_task(a, cur.nt);
         cur.raw = claim_raw(a, lane);
     }
 
@@ -645,17 +600,6 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
     int g0 = gather_src(a, q0, lane);
     Rec q1 = advance(a, cur, lane);
     uint32_t seq_issue = 0, seq_use = 0;
-    uint64_t ready = 0;   // dataflow: stages known finished (warp-uniform)
-    // may q0 be issued now?  (dataflow: the first op of a task waits for
-    // the stage it depends on; with ops still in flight it is deferred,
-    // with an empty ring the warp waits)
-    auto may_issue = [&](bool block) -> bool {
-        if (q0.dep < 0 || ((ready >> q0.dep) & 1)) return true;
-        if (block) wait_stage(a, q0.dep, lane);
-        else if (!stage_done(a, q0.dep, lane)) return false;
-        ready |= 1ull << q0.dep;
-        return true;
-    };
     auto issue_next = [&]() {
         issue<NR>(a, ring, seq_issue % kStages, q0, g0, lane);
         ++seq_issue;
@@ -663,7 +607,7 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
         g0 = gather_src(a, q0, lane);
         q1 = advance(a, cur, lane);
     };
-    while (q0.valid && seq_issue - seq_use < kStages && may_issue(seq_issue == seq_use)) issue_next();
+    while (q0.valid && seq_issue - seq_use < kStages) issue_next();
 
     // task accumulator: acc[grp][j] = slot 8j + lane/4, RHS 8grp + 2(lane%4)
     // .. +1, 64 slots (dense group tasks use the first 32)
@@ -765,16 +709,9 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
 #pragma unroll
                 for (int gr = 0; gr < G; ++gr) acc[gr][j][0] = acc[gr][j][1] = 0.0;
             }
-            if (a.flow) {
-                // publish: every lane's stores, then the stage count
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) atomicAdd(a.done + tm.w, 1);
-            }
         }
         __syncwarp();
-        while (q0.valid && seq_issue - seq_use < kStages && may_issue(seq_issue == seq_use))
-            issue_next();
+        while (q0.valid && seq_issue - seq_use < kStages) issue_next();
     }
 }
 
@@ -784,13 +721,9 @@ template <int NR>
 static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, double *arena,
                         cudaStream_t st, int max_ctas) {
     constexpr int W = Width<NR>::WARPS;
-    static bool attr_set = false;
     const size_t smem = sizeof(WarpRing<NR>) * W;
-    if (!attr_set) {
-        BF_CUDA(cudaFuncSetAttribute(alt_stage_kernel<NR>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
+    int rc = bf_ensure_smem((const void *)alt_stage_kernel<NR>, (int)smem);
+    if (rc) return rc;
     StageArgs a;
     a.tiles = pl->tiles;
     a.ops = pl->ops;
@@ -804,10 +737,6 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
     a.rec = pl->rec;
     a.xpos = pl->xpos;
     std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
-    a.flow = nullptr;
-    a.tinfo = nullptr;
-    a.done = nullptr;
-    a.need = nullptr;
     BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     int64_t want = (a.ntasks + W - 1) / W;
     const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;
@@ -840,109 +769,13 @@ int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) {
     return 0;
 }
 
-namespace {
-
-double stage_cost(const bfsht_plan *pl, int dir, int s) {
-    // proxy: tasks per stage weighted like the packer's LPT order; only
-    // used to split SMs between the chain and the free stage
-    const std::vector<int64_t> &b = pl->stages[dir];
-    return (double)(b[s + 1] - b[s]);
-}
-
-}  // namespace
-
-// The free stage (dense tiles, no device-side inputs) runs on a side stream
-// on its own SMs while the chain stages (butterfly factors, low-rank cores)
-// run on the caller's stream on the rest; the stages after it wait for both.
-// Each launch is persistent with one CTA per SM, so capping the two grids at
-// complementary CTA counts partitions the SMs between them.
-static int run_overlapped(bfsht_plan *pl, int dir, cudaStream_t st) {
-    const std::vector<int64_t> &b = pl->stages[dir];
-    const int nst = (int)b.size() - 1;
-    const int F = (int)pl->info[16 + dir];
-    if (!pl->side) {
-        BF_CUDA(cudaStreamCreateWithFlags(&pl->side, cudaStreamNonBlocking));
-        BF_CUDA(cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming));
-        BF_CUDA(cudaEventCreateWithFlags(&pl->ev_join, cudaEventDisableTiming));
-    }
-    // default split measured on B200 at N=1024 (scripts/tune_overlap.py):
-    // 40 of 148 SMs for the chain
-    const int chain_ctas = pl->chain_ctas > 0 ? pl->chain_ctas : (pl->sm_count * 27) / 100;
-    BF_CUDA(cudaEventRecord(pl->ev_fork, st));
-    BF_CUDA(cudaStreamWaitEvent(pl->side, pl->ev_fork, 0));
-    int rc = bf_run_stage(pl, b[F], b[F + 1], pl->counters + F, pl->side,
-                          pl->sm_count - chain_ctas);
-    if (rc) return rc;
-    BF_CUDA(cudaEventRecord(pl->ev_join, pl->side));
-    for (int s = 0; s < F; ++s) {
-        rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, chain_ctas);
-        if (rc) return rc;
-    }
-    BF_CUDA(cudaStreamWaitEvent(st, pl->ev_join, 0));
-    for (int s = F + 1; s < nst; ++s) {
-        rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, 0);
-        if (rc) return rc;
-    }
-    (void)stage_cost;
-    return 0;
-}
-
-// Dataflow schedule: the whole direction in one persistent launch, tasks
-// claimed in the packer's dataflow order (see packer.cpp build_flow).
-static int run_flow(bfsht_plan *pl, int dir, cudaStream_t st) {
-    constexpr int W = Width<BF_NRHS>::WARPS;
-    const std::vector<int64_t> &b = pl->stages[dir];
-    const int nst = (int)b.size() - 1;
-    if (nst > BFSHT_MAX_FLOW_STAGES) {
-        bfsht_set_error("too many stages for the dataflow schedule");
-        return -3;
-    }
-    static bool attr_set = false;
-    const size_t smem = sizeof(WarpRing<BF_NRHS>) * W;
-    if (!attr_set) {
-        BF_CUDA(cudaFuncSetAttribute(alt_stage_kernel<BF_NRHS>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-    }
-    int *ctr = pl->flow_ctr + dir * (BFSHT_MAX_FLOW_STAGES + 1);
-    StageArgs a;
-    a.tiles = pl->tiles;
-    a.ops = pl->ops;
-    a.idx = pl->idx;
-    a.maps = pl->maps;
-    a.tasks = pl->tasks;
-    a.arena = pl->arena;
-    a.t0 = 0;
-    a.ntasks = b[nst] - b[0];
-    a.counter = ctr;
-    a.rec = pl->rec;
-    a.xpos = pl->xpos;
-    std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
-    a.flow = pl->flow + (dir ? pl->stages[0].back() - pl->stages[0][0] : 0);
-    a.tinfo = pl->tinfo;
-    a.done = ctr + 1;
-    a.need = pl->flow_need + dir * BFSHT_MAX_FLOW_STAGES;
-    if (a.ntasks <= 0) return 0;
-    BF_CUDA(cudaMemsetAsync(ctr, 0, sizeof(int) * (BFSHT_MAX_FLOW_STAGES + 1), st));
-    // every CTA must be resident at once (tasks wait on other CTAs' tasks):
-    // one persistent CTA per SM, never more
-    alt_stage_kernel<BF_NRHS><<<pl->sm_count, W * 32, smem, st>>>(a);
-    BF_CUDA(cudaGetLastError());
-    pl->launches += 1;
-    return 0;
-}
-
 int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t st) {
-    if (pl->dataflow && pl->flow && pl->flow_ctr) return run_flow(pl, dir, st);
     const std::vector<int64_t> &b = pl->stages[dir];
     const int nst = (int)b.size() - 1;
     if (pl->ncounters < nst) {
         bfsht_set_error("plan counters not allocated");
         return -3;
     }
-    const int F = (int)pl->info[16 + dir];
-    const bool overlap = pl->overlap && F > 0 && F < nst && b[F + 1] > b[F];
-    if (overlap) return run_overlapped(pl, dir, st);
     for (int s = 0; s < nst; ++s) {
         int rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, 0);
         if (rc) return rc;

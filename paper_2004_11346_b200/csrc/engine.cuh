@@ -9,8 +9,6 @@
 #include "bfsht_b200.h"
 #include "format.h"
 
-#define BFSHT_MAX_FLOW_STAGES 62
-
 struct bfsht_plan {
     int64_t info[BFSHT_INFO_LEN];
     const double *tiles = nullptr;
@@ -19,12 +17,6 @@ struct bfsht_plan {
     const int8_t *maps = nullptr;
     const bf_task *tasks = nullptr;
     const bf_half *halves = nullptr;
-    const int32_t *flow = nullptr;    // dataflow claim order (fwd then inv)
-    const int32_t *tinfo = nullptr;   // per task: stage | (dep + 1) << 8
-    int *flow_ctr = nullptr;          // per direction: claim counter + done[stage]
-    int *flow_need = nullptr;         // per direction: tasks per stage
-    bool dataflow = false;            // schedule of bf_alt_apply (measured: staged is
-                                      // 1-2% faster at N=1024)
     const double *rec = nullptr;      // recurrence coefficients (regenerated tiles)
     const double *xpos = nullptr;     // positive nodes (regenerated tiles)
     // node-half addressing for the DFT stage: entry (order o, parity p, row r)
@@ -55,14 +47,34 @@ struct bfsht_plan {
     int64_t dft_scratch_rows = 0;
     int64_t launches = 0;
     int sm_count = 148;
-    // free-stage overlap (engine.cu run_overlapped)
-    bool overlap = true;
-    int chain_ctas = 0;               // 0: default split
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    int device = 0;                   // CUDA device the plan lives on
 };
 
 void bfsht_set_error(const std::string &msg);
+
+// Raise the dynamic shared-memory limit of kernel `func` on the CURRENT
+// device to at least `bytes` before a launch.  The attribute is per kernel
+// and per device context, so a per-(device, kernel) high-water mark is
+// kept: the limit only ever grows, and a launch never runs against a limit
+// another plan (or another device) set lower.  Thread-safe.
+int bf_ensure_smem(const void *func, int bytes);
+
+// Every entry point that takes a plan runs on the plan's device and leaves
+// the caller's current device as it found it.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(const bfsht_plan *pl) {
+        if (!pl) return;
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != pl->device) {
+            prev = cur;
+            cudaSetDevice(pl->device);
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
 
 #define BF_CUDA(call)                                                          \
     do {                                                                       \

@@ -62,7 +62,6 @@ struct bfsht_packed {
     int64_t n_bf = 0, n_lr = 0, n_dn = 0;
     int64_t n = 0, norders = 0;
     int32_t yr = 0;   // row-major forward node array Yr[r][order][parity]
-    int32_t free_stage[2] = {-1, -1};   // dependency-free dense stage per direction
     // regenerated dense tiles (f1)
     int64_t n_regen = 0, regen_values = 0;
     std::vector<double> rec;            // per order: (alpha, beta) for s = 0 .. 2N-m-1
@@ -392,100 +391,6 @@ struct Packer {
                 inv_groups[h_idx][gc].push_back(mk(BF_OP_TILE_T, t, hf.y + (int32_t)rr.first, R, C,
                                                    (int)(cc.first - (int64_t)gc * BF_T), flags, aux));
             }
-    }
-
-    // Dataflow schedule.  Every task gets its stage and the stage it depends
-    // on (the nearest non-empty earlier stage; -1 for none): butterfly /
-    // low-rank chain stages depend on their predecessor; a final group task
-    // depends on the chain only if one of its ops reads a chain output —
-    // "pure" group tasks (dense or low-rank-second-half tiles reading only
-    // the direction's inputs: forward coefficient halves, inverse node
-    // halves) depend on nothing; combine tasks depend on the group stage.
-    // The claim order interleaves the pure group tasks into the chain: each
-    // chain stage is spread over a share of them and followed by a gap of
-    // pure tasks long enough for the stage to finish before the next one is
-    // claimed, so no warp idles at a stage boundary and the latency-bound
-    // chain runs under the HBM-bound dense stream.  Every task with
-    // dependency d comes after all tasks of stage d in the order (no warp can
-    // wait on a task claimed after its own).
-    void build_flow(int G) {
-        P.tinfo.assign(P.tasks.size(), 0);
-        P.flow.clear();
-        if (P.free_stage[0] >= 0 || P.free_stage[1] >= 0) return;   // split schedule: staged only
-        const char *gap_env = std::getenv("BFSHT_FLOW_GAP");
-        const int64_t gap_tasks = gap_env ? std::atoll(gap_env) : 2 * 148 * 12;
-        for (int d = 0; d < 2; ++d) {
-            const auto &b = P.stage_bounds[d];
-            const int nst = (int)b.size() - 1;
-            const size_t f0 = P.flow.size();
-            std::vector<std::pair<int64_t, int64_t>> iv;
-            for (const bf_half &hf : P.halves)
-                if (hf.ncols > 0)
-                    iv.push_back(d == 0 ? std::make_pair((int64_t)hf.x, (int64_t)hf.x + hf.ncols)
-                                        : std::make_pair((int64_t)hf.y, (int64_t)hf.y + M.n));
-            std::sort(iv.begin(), iv.end());
-            auto is_input = [&](int64_t e) {
-                auto it = std::upper_bound(iv.begin(), iv.end(), std::make_pair(e, INT64_MAX));
-                if (it == iv.begin()) return false;
-                --it;
-                return e >= it->first && e < it->second;
-            };
-            auto pure = [&](const bf_task &t) {
-                for (int32_t i = 0; i < t.op_count; ++i) {
-                    const bf_op &o = P.ops[t.op_begin + i];
-                    if (o.kind == BF_OP_ADD || (o.flags & BF_OPF_GATHER)) return false;
-                    const int nvec = o.kind == BF_OP_TILE_N ? o.C : o.R;
-                    if (!is_input(o.in) || !is_input((int64_t)o.in + nvec - 1)) return false;
-                }
-                return true;
-            };
-            auto prev_nonempty = [&](int s) {
-                for (int q = s - 1; q >= 0; --q)
-                    if (b[q + 1] > b[q]) return q;
-                return -1;
-            };
-            std::vector<int32_t> pure_ids, mixed_ids, tail_ids;
-            std::vector<int> chain;
-            for (int s = 0; s < nst; ++s) {
-                if (s < G && b[s + 1] > b[s]) chain.push_back(s);
-                for (int64_t t = b[s]; t < b[s + 1]; ++t) {
-                    int dep = prev_nonempty(s);
-                    if (s == G) {
-                        if (pure(P.tasks[t])) {
-                            dep = -1;
-                            pure_ids.push_back((int32_t)t);
-                        } else {
-                            mixed_ids.push_back((int32_t)t);
-                        }
-                    } else if (s > G) {
-                        tail_ids.push_back((int32_t)t);
-                    }
-                    P.tinfo[t] = s | ((dep + 1) << 8);
-                }
-            }
-            const int64_t np = (int64_t)pure_ids.size();
-            const int64_t K = (int64_t)chain.size();
-            int64_t pi = 0;
-            for (int64_t j = 0; j < K; ++j) {
-                const int s = chain[j];
-                const int64_t budget = np * (j + 1) / (K + 1) - np * j / (K + 1);
-                const int64_t gap = std::min(budget, gap_tasks);
-                const int64_t mix = budget - gap;
-                const int64_t ns = b[s + 1] - b[s];
-                int64_t emitted = 0;
-                for (int64_t i = 0; i < ns; ++i) {
-                    P.flow.push_back((int32_t)(b[s] + i));
-                    const int64_t want = mix * (i + 1) / ns;
-                    for (; emitted < want; ++emitted) P.flow.push_back(pure_ids[pi++]);
-                }
-                for (int64_t g = 0; g < gap; ++g) P.flow.push_back(pure_ids[pi++]);
-            }
-            while (pi < np) P.flow.push_back(pure_ids[pi++]);
-            P.flow.insert(P.flow.end(), mixed_ids.begin(), mixed_ids.end());
-            P.flow.insert(P.flow.end(), tail_ids.begin(), tail_ids.end());
-            if ((int64_t)(P.flow.size() - f0) != b[nst] - b[0])
-                throw std::runtime_error("dataflow order is not a permutation of the tasks");
-        }
     }
 
     // Recurrence-coefficient tables and per-row seeds of the regenerated
@@ -889,27 +794,13 @@ struct Packer {
                      (int32_t)std::min<int64_t>(BF_T, hf.ncols - (int64_t)g * BF_T),
                      std::move(inv_groups[hi][g]), std::move(inv_other[hi][g])});
         }
-        // Stage layout per direction:
-        //   0 .. last-1   chain: butterfly factors and low-rank cores
-        //   F = last      free: dense tiles only (no device-side inputs), run
-        //                 concurrently with the chain on its own SMs
-        //   X = last + 1  fix-up: dense partials + low-rank (u s) t / v t
-        //                 tiles + butterfly block outputs
-        //   C = last + 2  combine (only for fix-ups longer than kMaxTaskOps)
-        // Dense tiles hold ~85% of the bytes and stream at the HBM roofline;
-        // overlapping them with the latency-bound chain hides the chain.
-        // Long op lists (e.g. the single column group of a half with a few
-        // columns, which collects every block of a tall thin matrix) are
-        // chunked into partial sums so no task runs long on one warp.  The
-        // summation order is fixed here, so results are bitwise reproducible.
-        //
-        // Measured on B200 (N=1024, scripts/tune_overlap.py): the overlap
-        // saves ~65 us per direction but the extra fix-up stage of small
-        // tasks costs ~130 us, so by default every group task runs in the
-        // final stage (F = X); BFSHT_SPLIT_FREE=1 selects the split schedule.
-        const char *split_env = std::getenv("BFSHT_SPLIT_FREE");
-        const bool split = split_env && std::atoi(split_env) != 0;
-        if (!split) {
+        // Every group task runs in the final stage (measured on B200 at
+        // N=1024: dealing the dependency-free dense tiles over the chain
+        // stages, or running them on a side stream, cost more in extra
+        // fix-up work than it hid); long op lists are chunked into partial
+        // sums + a combine stage.  The summation order is fixed here, so
+        // results are bitwise reproducible.
+        {
             for (int d = 0; d < 2; ++d) {
                 for (auto &gp : groups[d]) {
                     std::vector<bf_op> ops = std::move(gp.dense);
@@ -935,42 +826,6 @@ struct Packer {
             groups[0].clear();
             groups[1].clear();
         }
-        const int F = last, X = last + 1, C = last + 2;
-        for (int d = 0; d < 2 && split; ++d) {
-            stage(d, X);
-            for (auto &gp : groups[d]) {
-                const int nout = gp.nout & 0xff;
-                const size_t nd = gp.dense.size();
-                if (gp.other.empty() && nd <= (size_t)kMaxTaskOps) {
-                    add_task(d, nd ? F : X, gp.out, gp.nout, std::move(gp.dense));
-                    continue;
-                }
-                std::vector<bf_op> fix;
-                for (size_t b = 0; b < nd; b += kMaxTaskOps) {
-                    const size_t e = std::min(nd, b + kMaxTaskOps);
-                    const int32_t part = alloc_entries(nout);
-                    add_task(d, F, part, nout,
-                             std::vector<bf_op>(gp.dense.begin() + b, gp.dense.begin() + e));
-                    for (int h0 = 0; h0 < nout; h0 += BF_T)
-                        fix.push_back(mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
-                }
-                fix.insert(fix.end(), gp.other.begin(), gp.other.end());
-                if (fix.size() <= (size_t)kMaxTaskOps) {
-                    add_task(d, X, gp.out, gp.nout, std::move(fix));
-                    continue;
-                }
-                std::vector<bf_op> comb;
-                for (size_t b = 0; b < fix.size(); b += kMaxTaskOps) {
-                    const size_t e = std::min(fix.size(), b + kMaxTaskOps);
-                    const int32_t part = alloc_entries(nout);
-                    add_task(d, X, part, nout, std::vector<bf_op>(fix.begin() + b, fix.begin() + e));
-                    for (int h0 = 0; h0 < nout; h0 += BF_T)
-                        comb.push_back(mk(BF_OP_ADD, 0, part + h0, std::min(BF_T, nout - h0), 0, h0));
-                }
-                add_task(d, C, gp.out, gp.nout, std::move(comb));
-            }
-            P.free_stage[d] = F;
-        }
         // flatten: stages in order, tasks by descending cost
         for (int d = 0; d < 2; ++d) {
             P.stage_bounds[d].clear();
@@ -991,7 +846,6 @@ struct Packer {
                 P.stage_bounds[d].push_back((int64_t)P.tasks.size());
             }
         }
-        build_flow(last);
         // fill tiles
         const int64_t nj = (int64_t)jobs.size();
         P.tiles.reset(new double[(size_t)std::max<int64_t>(P.n_tiles, 2)]);
@@ -1034,8 +888,7 @@ extern "C" int bfsht_pack_plan(const bfsht_manifest *man, int threads, bfsht_pac
 extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_LEN]) {
     if (!p) return -1;
     std::memset(info, 0, BFSHT_INFO_LEN * sizeof(int64_t));
-    info[16] = p->free_stage[0];
-    info[17] = p->free_stage[1];
+    info[16] = info[17] = -1;   // reserved (no split free stage)
     info[0] = p->n_tiles;
     info[1] = (int64_t)p->ops.size();
     info[2] = (int64_t)p->idx.size();
@@ -1057,14 +910,13 @@ extern "C" int bfsht_packed_info(const bfsht_packed *p, int64_t info[BFSHT_INFO_
     info[20] = (int64_t)p->rec.size();
     info[21] = (int64_t)p->xpos.size();
     std::memcpy(&info[22], &p->mag_min, sizeof(double));
-    info[23] = (int64_t)p->flow.size();
+    info[23] = 0;               // reserved (no dataflow order)
     return 0;
 }
 
 // arrays: 0 tiles, 1 ops, 2 idx, 3 maps, 4 tasks, 5 halves,
 //         6 stage bounds fwd (int64, stages+1), 7 stage bounds inv,
-//         8 recurrence coefficients, 9 x_pos, 10 dataflow order (fwd
-//         then inv task ids), 11 per-task stage | (dep + 1) << 8
+//         8 recurrence coefficients, 9 x_pos, 10 / 11 reserved (NULL)
 extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]) {
     if (!p) return -1;
     arrays[0] = p->tiles.get();
@@ -1077,8 +929,8 @@ extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]
     arrays[7] = p->stage_bounds[1].data();
     arrays[8] = p->rec.data();
     arrays[9] = p->xpos.data();
-    arrays[10] = p->flow.data();
-    arrays[11] = p->tinfo.data();
+    arrays[10] = nullptr;
+    arrays[11] = nullptr;
     return 0;
 }
 

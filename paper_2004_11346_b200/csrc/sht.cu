@@ -834,8 +834,15 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
                 wt.push_back(w[2 * e + 1]);
             }
     }
-    for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw})
+    // re-prepare for a new length: every table and the scratch of the old one go
+    for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
+                    (void *)pl->dft_scratch})
         if (p) cudaFree(p);
+    pl->dft_w = pl->dft_tw = nullptr;
+    pl->dft_perm = nullptr;
+    pl->dft_scratch = nullptr;
+    pl->dft_scratch_rows = 0;
+    pl->dft_L = 0;
     BF_CUDA(cudaMalloc(&pl->dft_w, 8 * wt.size()));
     BF_CUDA(cudaMalloc(&pl->dft_tw, 16 * L));
     BF_CUDA(cudaMalloc(&pl->dft_perm, 4 * L));
@@ -848,27 +855,13 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     const int gen = pl->dft_gen;
     const int need = dft_smem_bytes(L, 2);
     int maxsm = 0;
-    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
-    if (gen > 0) {
-        // global-scratch variants: their dynamic shared memory is the staging
-        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
-        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
-        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, gen));
-    }
+    BF_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
     if (need + gen > maxsm) {
         const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
         BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * L * rows));
         pl->dft_scratch_rows = rows;
-    } else {
-        const int pair = dft_pair_smem(L, gen);
-        BF_CUDA(cudaFuncSetAttribute(sht_synth_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair));
-        BF_CUDA(cudaFuncSetAttribute(sht_anal_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     std::max(pair, dft_anal_smem(L, 2 * (int64_t)pl->norders, gen))));
-        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     std::min(dft_smem_bytes(L, 1) + gen, 227 * 1024)));
-        BF_CUDA(cudaFuncSetAttribute(dft_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     dft_smem_bytes(L, 1)));
     }
+    // dynamic shared-memory limits are raised per launch (bf_ensure_smem)
     return 0;
 }
 
@@ -890,11 +883,17 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const bool sm = pl->dft_scratch == nullptr;
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
+    {
+        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
+        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+        if (rc_) return rc_;
+        kern_<<<nblk, kDftThreads, smem_, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), pl->info[10],
         2 * pl->norders, BF_NRHS);
+    }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -910,11 +909,17 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     const int64_t nh = 2 * (int64_t)pl->norders;
     const bool ysm = sm && dft_y_smem(pl->dft_L, nh, pl->dft_gen);
-    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(pl->dft_L, nh, pl->dft_gen) : dft_pair_smem(pl->dft_L, pl->dft_gen)) : pl->dft_gen, st>>>(
+    {
+        const int smem_ = sm ? (ysm ? dft_anal_smem(pl->dft_L, nh, pl->dft_gen) : dft_pair_smem(pl->dft_L, pl->dft_gen)) : pl->dft_gen;
+        auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
+        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+        if (rc_) return rc_;
+        kern_<<<nblk, kDftThreads, smem_, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
         weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen),
         ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS);
+    }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
@@ -1138,13 +1143,19 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
         rc = bf_alt_apply_wide(pl, BFSHT_FORWARD, work, st);
         if (rc) return rc;
         for (int b = 0; b < B; ++b) {
-            (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(L, pl->dft_gen) : pl->dft_gen, st>>>(
+            {
+                const int smem_ = sm ? dft_pair_smem(L, pl->dft_gen) : pl->dft_gen;
+                auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
+                int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+                if (rc_) return rc_;
+                kern_<<<nblk, kDftThreads, smem_, st>>>(
                 d, n, pl->layout_fwd, work + BF_NRHS * b, 0, n,
                 reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<double2 *>(out) + b * ngrid, sm,
                 reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen), pl->info[10],
                 2 * pl->norders, ew);
+            }
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
         }
@@ -1152,13 +1163,19 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
         const int64_t nh = 2 * (int64_t)pl->norders;
         const bool ysm = sm && dft_y_smem(L, nh, pl->dft_gen);
         for (int b = 0; b < B; ++b) {
-            (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? (ysm ? dft_anal_smem(L, nh, pl->dft_gen) : dft_pair_smem(L, pl->dft_gen)) : pl->dft_gen, st>>>(
+            {
+                const int smem_ = sm ? (ysm ? dft_anal_smem(L, nh, pl->dft_gen) : dft_pair_smem(L, pl->dft_gen)) : pl->dft_gen;
+                auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
+                int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+                if (rc_) return rc_;
+                kern_<<<nblk, kDftThreads, smem_, st>>>(
                 d, n, pl->layout_inv, work + BF_NRHS * b,
                 reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<const double2 *>(in) + b * ngrid, weights, 0, n, sm,
                 reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen),
                 ysm ? pl->node_y : nullptr, (int)nh, ew);
+            }
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
         }
@@ -1186,7 +1203,10 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
     // footprint (2 CTAs per SM) for the all-templated lengths
     auto kern = sm ? (pl->dft_gen ? dft_rows_kernel<true, true> : dft_rows_kernel<true, false>)
                    : (pl->dft_gen ? dft_rows_kernel<false, true> : dft_rows_kernel<false, false>);
-    kern<<<grid, kDftThreads, sm ? dft_smem_bytes(L, 1) + pl->dft_gen : pl->dft_gen, st>>>(
+    const int smem = sm ? dft_smem_bytes(L, 1) + pl->dft_gen : pl->dft_gen;
+    rc = bf_ensure_smem((const void *)kern, smem);
+    if (rc) return rc;
+    kern<<<grid, kDftThreads, smem, st>>>(
         make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
         reinterpret_cast<double2 *>(pl->dft_scratch));
@@ -1203,11 +1223,17 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_synth_kernel<true> : sht_synth_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
+    {
+        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
+        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+        if (rc_) return rc_;
+        kern_<<<nblk, kDftThreads, smem_, st>>>(
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
         reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), (int64_t)0, 0, BF_NRHS);
+    }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -1221,11 +1247,17 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     if (r_count <= 0) return 0;
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    (sm ? sht_anal_kernel<true> : sht_anal_kernel<false>)<<<nblk, kDftThreads, sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen, st>>>(
+    {
+        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
+        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
+        if (rc_) return rc_;
+        kern_<<<nblk, kDftThreads, smem_, st>>>(
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
         reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), nullptr, 0, BF_NRHS);
+    }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;

@@ -369,6 +369,20 @@ class ShardedSht(_Common):
                 parts.append(flat[start:start + 2 * n - abs(mm)])
         return np.concatenate(parts)
 
+    def unshard_coeffs(self, shard, total):
+        """Shard-layout coefficients back into a flat ShtCoeffs.pack() array
+        (orders of other ranks left zero)."""
+        n = self.n
+        out = np.zeros(total, dtype=np.complex128)
+        at = 0
+        for m in self.orders:
+            for mm in ((m, -m) if m else (m,)):
+                ln = 2 * n - abs(mm)
+                start = _flat_offset(n, mm)
+                out[start:start + ln] = shard[at:at + ln]
+                at += ln
+        return out
+
     def shard_grid(self, full):
         n = self.n
         r0, r1 = self.r0, self.r0 + self.rc

@@ -416,6 +416,19 @@ def _plan_orders(args):
     return out, path
 
 
+def _start_method():
+    """fork is cheapest, but forking a process whose CUDA / NCCL threads are
+    running can deadlock the child: use forkserver once CUDA is up."""
+    import sys
+    torch = sys.modules.get("torch")
+    try:
+        if torch is not None and torch.cuda.is_initialized():
+            return "forkserver"
+    except Exception:
+        pass
+    return "fork"
+
+
 def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
                 processes=1, quadrature=None):
     """Plans for an arbitrary list of orders (one shard of an SHT), built in
@@ -441,7 +454,7 @@ def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
                     f"planning failed at order m={m}: {exc}") from exc
         return plans
     import multiprocessing as mp
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context(_start_method())
     chunks = [orders[r::p] for r in range(p)]
     spill = _spill_dir()
     with ctx.Pool(p) as pool:

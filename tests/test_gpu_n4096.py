@@ -21,7 +21,7 @@ def rel(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-@pytest.mark.parametrize("n,ms", [(4096, [2048, 5000, 8100, 8191]),
+@pytest.mark.parametrize("n,ms", [(4096, [0, 1, 2048, 5000, 8100, 8191]),
                                   (8192, [16000, 16383])])
 def test_large_n_sampled_orders(n, ms):
     from paper_2004_11346_b200.api import DevicePlan, FORWARD, INVERSE

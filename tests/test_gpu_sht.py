@@ -87,3 +87,24 @@ def test_sht_batch_bitwise(n, batch):
         assert torch.equal(g[b], gs)
         assert torch.equal(back[b], dev.inverse(gs))
     assert rel(back.cpu().numpy(), flats) < 1e-11
+
+
+def test_plan_reuse_after_smaller_length():
+    # the DFT kernels' dynamic shared-memory limit is per kernel: a small-L
+    # plan (or a standalone dft_rows call) in between must not break a later
+    # launch of a large-L plan (the limit used to be lowered)
+    import torch
+    from paper_2004_11346_b200 import SamplingConfig, plan_orders
+    from paper_2004_11346_b200.api import DevicePlan, dft_rows
+    n = 1024
+    plans = plan_orders(n, range(2 * n), SamplingConfig(tolerance=1e-12), processes=0)
+    big = DevicePlan(plans, weights=plans[0].quadrature.weights)
+    c = torch.from_numpy(random_flat(n, 5)).cuda()
+    g1 = big.sht_forward(c)
+    small = DevicePlan(plan_sht(64).alt_plans, weights=plan_sht(64).quadrature.weights)
+    small.sht_forward(torch.from_numpy(random_flat(64, 6)).cuda())
+    dft_rows(torch.zeros((3, 15), dtype=torch.complex128, device="cuda"))
+    g2 = big.sht_forward(c)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2)
+    assert torch.equal(big.sht_inverse(g1), big.sht_inverse(g2))
