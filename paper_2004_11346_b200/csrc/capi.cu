@@ -206,7 +206,7 @@ void bfsht_plan_free(bfsht_plan *pl) {
     if (cur != pl->device) cudaSetDevice(pl->device);
     for (void *p : pl->owned) cudaFree(p);
     for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
-                    (void *)pl->dft_scratch})
+                    (void *)pl->dft_scratch, (void *)pl->dft_chirp, (void *)pl->dft_hhat})
         if (p) cudaFree(p);
     if (cur != pl->device) cudaSetDevice(cur);
     delete pl;

@@ -37,7 +37,11 @@ struct bfsht_plan {
     // per-order API scratch
     int64_t *order_off = nullptr;     // device, 2*norders+2 offsets
     // DFT tables (built lazily for L = 4N-1)
-    int64_t dft_L = 0;
+    int64_t dft_L = 0;                // transform length
+    int64_t dft_Lb = 0;               // row buffer length (L, or Bluestein M)
+    bool dft_blue = false;            // Bluestein rows
+    double *dft_chirp = nullptr;      // Bluestein: L complex exp(-i pi j^2/L)
+    double *dft_hhat = nullptr;       // Bluestein: M complex FFT_M(conj chirp)/M
     double *dft_w = nullptr;          // pass twiddle table (L complex) + radix roots
     int32_t *dft_perm = nullptr;      // digit-reversal positions
     double *dft_tw = nullptr;         // L complex: exp(i m phi0) per bin

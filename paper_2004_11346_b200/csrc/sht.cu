@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <algorithm>
 #include <complex>
 #include <vector>
@@ -34,7 +35,9 @@ constexpr int kMaxRadix = 24;
 constexpr int kDftThreads = BF_DFT_THREADS;
 
 struct DftDesc {
-    int L;
+    int L;       // transform length
+    int Lb;      // row buffer length: L, or the Bluestein convolution length M
+    int blue;    // 1: Bluestein (chirp-z) rows of length M >= 2L-1
     int nrad;
     int radix[kMaxRadix];
     // per pass: exact multiplicative inverse of the pass's span (the product
@@ -46,6 +49,7 @@ struct DftDesc {
     // twiddle loads are consecutive) and of its P radix roots
     int tw_off[kMaxRadix];
     int root_off[kMaxRadix];
+    int span[kMaxRadix];
 };
 
 __device__ __forceinline__ int fast_div(int x, unsigned inv) {
@@ -70,7 +74,14 @@ __device__ __forceinline__ double2 conjif(double2 a, bool c) {
 //   y_s, y_{P-s} = x_0 + sum_j a_j cos(2 pi js/P)  +/-  i sum_j b_j sin(..)
 // (signs per direction), about a quarter of the P^2 complex products of a
 // naive size-P DFT.
-template <int P>
+//
+// DIF = false: decimation in time (twiddle the inputs, then the butterfly;
+// passes in radix order, input digit-reversed, output natural).  DIF =
+// true: the transposed pass (butterfly, then twiddle the outputs; passes
+// in reverse order, input natural, output digit-reversed) — the DFT matrix
+// is symmetric, so the transposed pass sequence computes the same DFT.
+// Bluestein rows use both (see row_dft).
+template <int P, bool DIF = false>
 __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int span,
                                            unsigned span_inv, const double2 *Tw,
                                            const double2 *__restrict__ R, bool inv) {
@@ -91,41 +102,60 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
         double2 x[P];
 #pragma unroll
         for (int q = 0; q < P; ++q) x[q] = row[base + q * span];
-        if (span > 1) {
+        if (!DIF && span > 1) {
 #pragma unroll
             for (int q = 1; q < P; ++q) x[q] = cmul(x[q], conjif(Tw[(q - 1) * span + k], inv));
         }
+        double2 y[P];
         if (P == 2) {
-            row[base] = make_double2(x[0].x + x[1].x, x[0].y + x[1].y);
-            row[base + span] = make_double2(x[0].x - x[1].x, x[0].y - x[1].y);
-            continue;
-        }
-        constexpr int H = (P - 1) / 2;
-        double2 a[H + 1], bb[H + 1];
-        double2 y0 = x[0];
-#pragma unroll
-        for (int j = 1; j <= H; ++j) {
-            a[j] = make_double2(x[j].x + x[P - j].x, x[j].y + x[P - j].y);
-            bb[j] = make_double2(x[j].x - x[P - j].x, x[j].y - x[P - j].y);
-            y0.x += a[j].x;
-            y0.y += a[j].y;
-        }
-        row[base] = y0;
-#pragma unroll
-        for (int sidx = 1; sidx <= H; ++sidx) {
-            double2 re = x[0], im = make_double2(0.0, 0.0);
+            y[0] = make_double2(x[0].x + x[1].x, x[0].y + x[1].y);
+            y[1] = make_double2(x[0].x - x[1].x, x[0].y - x[1].y);
+        } else if (P == 4) {
+            // W = -i (forward) / +i (inverse)
+            const double2 s02 = make_double2(x[0].x + x[2].x, x[0].y + x[2].y);
+            const double2 d02 = make_double2(x[0].x - x[2].x, x[0].y - x[2].y);
+            const double2 s13 = make_double2(x[1].x + x[3].x, x[1].y + x[3].y);
+            const double2 d13 = make_double2(x[1].x - x[3].x, x[1].y - x[3].y);
+            // -i * d13 = (d13.y, -d13.x)
+            const double2 r = inv ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);
+            y[0] = make_double2(s02.x + s13.x, s02.y + s13.y);
+            y[2] = make_double2(s02.x - s13.x, s02.y - s13.y);
+            y[1] = make_double2(d02.x + r.x, d02.y + r.y);
+            y[3] = make_double2(d02.x - r.x, d02.y - r.y);
+        } else {
+            constexpr int H = (P - 1) / 2;
+            double2 a[H + 1], bb[H + 1];
+            double2 y0 = x[0];
 #pragma unroll
             for (int j = 1; j <= H; ++j) {
-                const int t = (j * sidx) % P;
-                re.x = fma(a[j].x, cr[t], re.x);
-                re.y = fma(a[j].y, cr[t], re.y);
-                im.x = fma(bb[j].x, ci[t], im.x);
-                im.y = fma(bb[j].y, ci[t], im.y);
+                a[j] = make_double2(x[j].x + x[P - j].x, x[j].y + x[P - j].y);
+                bb[j] = make_double2(x[j].x - x[P - j].x, x[j].y - x[P - j].y);
+                y0.x += a[j].x;
+                y0.y += a[j].y;
             }
-            // x_j w^{js} + x_{P-j} w^{-js} = a_j cr + i ci b_j
-            row[base + sidx * span] = make_double2(re.x - im.y, re.y + im.x);
-            row[base + (P - sidx) * span] = make_double2(re.x + im.y, re.y - im.x);
+            y[0] = y0;
+#pragma unroll
+            for (int sidx = 1; sidx <= H; ++sidx) {
+                double2 re = x[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 1; j <= H; ++j) {
+                    const int t = (j * sidx) % P;
+                    re.x = fma(a[j].x, cr[t], re.x);
+                    re.y = fma(a[j].y, cr[t], re.y);
+                    im.x = fma(bb[j].x, ci[t], im.x);
+                    im.y = fma(bb[j].y, ci[t], im.y);
+                }
+                // x_j w^{js} + x_{P-j} w^{-js} = a_j cr + i ci b_j
+                y[sidx] = make_double2(re.x - im.y, re.y + im.x);
+                y[P - sidx] = make_double2(re.x + im.y, re.y - im.x);
+            }
         }
+        if (DIF && span > 1) {
+#pragma unroll
+            for (int q = 1; q < P; ++q) y[q] = cmul(y[q], conjif(Tw[(q - 1) * span + k], inv));
+        }
+#pragma unroll
+        for (int q = 0; q < P; ++q) row[base + q * span] = y[q];
     }
 }
 
@@ -290,21 +320,21 @@ __device__ void generic_pass(double2 *buf, int nrows, int L, int span, int P, co
     }
 }
 
-// All passes over `nrows` rows of buf (row stride L), whole CTA.  Tw: the
-// pass twiddle table (L entries, shared or global memory); R: radix roots.
+// All passes over `nrows` rows of buf (row stride Lb), whole CTA.  Tw: the
+// pass twiddle table (Lb entries, shared or global memory); R: radix roots.
 template <bool GEN = true>
 __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const double2 *Tw,
                            const double2 *__restrict__ R, bool inv) {
-    const int L = d.L;
-    int span = 1;
+    const int L = d.Lb;
     for (int ri = 0; ri < d.nrad; ++ri) {
-        const int P = d.radix[ri];
+        const int P = d.radix[ri], span = d.span[ri];
         const unsigned si = d.span_inv[ri];
         const double2 *tw = Tw + d.tw_off[ri];
         const double2 *rr = R + d.root_off[ri];
         switch (P) {
             case 2: radix_pass<2>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 3: radix_pass<3>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 4: radix_pass<4>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 5: radix_pass<5>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 7: radix_pass<7>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 11: radix_pass<11>(buf, nrows, L, span, si, tw, rr, inv); break;
@@ -314,8 +344,63 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const doub
                 else __trap();   // launched without the generic radix (host picks by radices)
         }
         __syncthreads();
-        span *= P;
     }
+}
+
+// The transposed pass sequence (DIF): natural-order input, output at the
+// digit-reversed positions perm[k].  Bluestein lengths are 2-3-5-7-smooth,
+// so only templated radices occur.
+__device__ void dft_passes_dif(double2 *buf, int nrows, const DftDesc &d, const double2 *Tw,
+                               const double2 *__restrict__ R, bool inv) {
+    const int L = d.Lb;
+    for (int ri = d.nrad - 1; ri >= 0; --ri) {
+        const int P = d.radix[ri], span = d.span[ri];
+        const unsigned si = d.span_inv[ri];
+        const double2 *tw = Tw + d.tw_off[ri];
+        const double2 *rr = R + d.root_off[ri];
+        switch (P) {
+            case 2: radix_pass<2, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 3: radix_pass<3, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 4: radix_pass<4, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 5: radix_pass<5, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 7: radix_pass<7, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            default: __trap();
+        }
+        __syncthreads();
+    }
+}
+
+// Length-L DFT of `nrows` rows already scattered into buf (digit-reversed
+// positions perm[j], j < L; for Bluestein rows pre-multiplied by the chirp
+// and zero at every other position).  Direct rows: mixed-radix DIT, result
+// in natural order.  Bluestein rows (Bluestein 1970 / Rabiner-Schafer-Rader
+// chirp-z: jk = (j^2 + k^2 - (k-j)^2)/2, so y_k = c_k sum_j (x_j c_j)
+// conj(c_{k-j}) with c_j = exp(-i pi j^2/L), a cyclic convolution of length
+// M >= 2L-1): forward DIT FFT of length M, times H = FFT_M(conj c)/M
+// (conjugated for the +i direction), inverse DIF FFT; the convolution lands
+// at positions perm[k], to be multiplied by c_k (or conj c_k) on the way out.
+template <bool GEN>
+__device__ __forceinline__ void row_dft(double2 *buf, int nrows, const DftDesc &d,
+                                        const double2 *Tw, const double2 *__restrict__ R,
+                                        const double2 *__restrict__ H, bool inv) {
+    if (!d.blue) {
+        dft_passes<GEN>(buf, nrows, d, Tw, R, inv);
+        return;
+    }
+    dft_passes<false>(buf, nrows, d, Tw, R, false);
+    const int M = d.Lb;
+    for (int rw = 0; rw < nrows; ++rw)
+        for (int i = threadIdx.x; i < M; i += blockDim.x)
+            buf[(int64_t)rw * M + i] = cmul(buf[(int64_t)rw * M + i], conjif(H[i], inv));
+    __syncthreads();
+    dft_passes_dif(buf, nrows, d, Tw, R, true);
+}
+
+// Zero the rows of a Bluestein buffer before the input scatter.
+__device__ __forceinline__ void row_clear(double2 *buf, int nrows, const DftDesc &d) {
+    if (!d.blue) return;
+    for (int i = threadIdx.x; i < nrows * d.Lb; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+    __syncthreads();
 }
 
 // SM is a template argument so that, once inlined, every row access is a
@@ -332,16 +417,21 @@ template <bool SM, bool GEN>
 __global__ void __launch_bounds__(kDftThreads, 2) dft_rows_kernel(
     DftDesc d, const double2 *__restrict__ in, double2 *__restrict__ out, int64_t rows,
     const int *__restrict__ perm, const double2 *__restrict__ W, bool inv, bool use_smem,
-    double2 *scratch) {
-    const int L = d.L;
-    double2 *buf = dft_buffer<SM>(scratch, 1, L);
+    double2 *scratch, const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
+    const int L = d.L, Lb = d.Lb;
+    double2 *buf = dft_buffer<SM>(scratch, 1, Lb);
     for (int64_t rw = blockIdx.x; rw < rows; rw += gridDim.x) {
         const double2 *src = in + rw * L;
-        for (int j = threadIdx.x; j < L; j += blockDim.x) buf[perm[j]] = src[j];
+        row_clear(buf, 1, d);
+        for (int j = threadIdx.x; j < L; j += blockDim.x) {
+            const double2 v = src[j];
+            buf[perm[j]] = d.blue ? cmul(v, conjif(chirp[j], inv)) : v;
+        }
         __syncthreads();
-        dft_passes<GEN>(buf, 1, d, W, W + L, inv);
+        row_dft<GEN>(buf, 1, d, W, W + Lb, H, inv);
         double2 *dst = out + rw * L;
-        for (int j = threadIdx.x; j < L; j += blockDim.x) dst[j] = buf[j];
+        for (int j = threadIdx.x; j < L; j += blockDim.x)
+            dst[j] = d.blue ? cmul(buf[perm[j]], conjif(chirp[j], inv)) : buf[j];
         __syncthreads();
     }
 }
@@ -352,7 +442,8 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
     int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
-    double2 *scratch, bool w_smem, int64_t yr, int ystride, int ew) {
+    double2 *scratch, bool w_smem, int64_t yr, int ystride, int ew,
+    const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
     // ystride > 0 (whole-SHT path): entry (order am, parity p, row rr) sits
     // at yr + rr * ystride + 2 am + p in the row-major node array Yr, and
     // absent halves read as zeros there (never written), so no layout-table
@@ -361,19 +452,20 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
     // grid holds 2*r_count local rows: lower rows n-r_begin-r_count .. n-r_begin-1
     // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
     // r_begin = 0, r_count = n)
-    const int L = d.L;
-    double2 *buf = dft_buffer<SM>(scratch, 2, L);
+    const int L = d.L, Lb = d.Lb;
+    double2 *buf = dft_buffer<SM>(scratch, 2, Lb);
     // twiddle table next to the rows in shared memory when it fits
     const double2 *Wt = W;
     if (SM && w_smem) {
-        double2 *ws = buf + 2 * L;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
+        double2 *ws = buf + 2 * Lb;
+        for (int i = threadIdx.x; i < Lb; i += blockDim.x) ws[i] = W[i];
         __syncthreads();
         Wt = ws;
     }
     const int mtop = 2 * n - 1;
     for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
     const int rr = r - r_begin;
+    row_clear(buf, 2, d);
     // one thread per order |m|: its odd and even node-half entries (+m and
     // -m, 32 B each, adjacent in Yr) are read whole and feed the two bins
     // m and L-m of both rows, so every loaded sector is fully used; orders
@@ -402,6 +494,10 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
                 const int bn = am > 0 ? L - am : 0;
                 tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
                 tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+                if (d.blue && ok) {
+                    tp[i] = cmul(tp[i], conjif(chirp[am], true));
+                    tn[i] = cmul(tn[i], conjif(chirp[bn], true));
+                }
                 pp[i] = ok ? perm[am] : 0;
                 pn[i] = ok ? perm[bn] : 0;
             }
@@ -433,6 +529,10 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
             const int bn = am > 0 && ok ? L - am : 0;
             tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
             tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+            if (d.blue && ok) {
+                tp[i] = cmul(tp[i], conjif(chirp[am], true));
+                tn[i] = cmul(tn[i], conjif(chirp[bn], true));
+            }
             pp[i] = ok ? perm[am] : 0;
             pn[i] = ok ? perm[bn] : 0;
         }
@@ -442,16 +542,16 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
             const int am = a0 + i * blockDim.x;
             if (am < nord) {
                 buf[pp[i]] = cmul(make_double2(ep[i].x + op[i].x, ep[i].y + op[i].y), tp[i]);
-                buf[L + pp[i]] = cmul(make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y), tp[i]);
+                buf[Lb + pp[i]] = cmul(make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y), tp[i]);
                 if (am > 0) {
                     buf[pn[i]] = cmul(make_double2(en[i].x + on[i].x, en[i].y + on[i].y), tn[i]);
-                    buf[L + pn[i]] = cmul(make_double2(en[i].x - on[i].x, en[i].y - on[i].y), tn[i]);
+                    buf[Lb + pn[i]] = cmul(make_double2(en[i].x - on[i].x, en[i].y - on[i].y), tn[i]);
                 }
             }
         }
     }
     __syncthreads();
-    dft_passes(buf, 2, d, Wt, W + L, true);
+    row_dft<true>(buf, 2, d, Wt, W + Lb, H, true);
     double2 *up = grid + (int64_t)(r_count + rr) * L;
     double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
     // batched so several (scratch-path: L2) loads are in flight per thread
@@ -461,8 +561,14 @@ __global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
         for (int u = 0; u < 4; ++u) {
             const int j = j0 + u * blockDim.x;
             if (j < L) {
-                vu[u] = buf[j];
-                vl[u] = buf[L + j];
+                const int pj = d.blue ? perm[j] : j;
+                vu[u] = buf[pj];
+                vl[u] = buf[Lb + pj];
+                if (d.blue) {
+                    const double2 c = conjif(chirp[j], true);
+                    vu[u] = cmul(vu[u], c);
+                    vl[u] = cmul(vl[u], c);
+                }
             }
         }
 #pragma unroll
@@ -485,21 +591,22 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const double2 *__restrict__ tw, const int *__restrict__ perm,
     const double2 *__restrict__ W, const double2 *__restrict__ grid,
     const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
-    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny, int ew) {
-    const int L = d.L;
-    double2 *buf = dft_buffer<SM>(scratch, 2, L);
+    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny, int ew,
+    const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
+    const int L = d.L, Lb = d.Lb;
+    double2 *buf = dft_buffer<SM>(scratch, 2, Lb);
     // twiddle table next to the rows in shared memory when it fits
     const double2 *Wt = W;
     if (SM && w_smem) {
-        double2 *ws = buf + 2 * L;
-        for (int i = threadIdx.x; i < L; i += blockDim.x) ws[i] = W[i];
+        double2 *ws = buf + 2 * Lb;
+        for (int i = threadIdx.x; i < Lb; i += blockDim.x) ws[i] = W[i];
         Wt = ws;
     }
     // whole-SHT path: node-half bases (-1 = absent half) staged in shared
     // memory after the twiddles, replacing per-bin layout-table loads
     int *ys = nullptr;
     if (SM && w_smem && node_y) {
-        ys = reinterpret_cast<int *>(buf + 3 * L);
+        ys = reinterpret_cast<int *>(buf + 3 * Lb);
         for (int i = threadIdx.x; i < ny; i += blockDim.x) ys[i] = node_y[i];
     }
     __syncthreads();
@@ -507,6 +614,7 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     const int rr = r - r_begin;
     const double2 *up = grid + (int64_t)(r_count + rr) * L;
     const double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
+    row_clear(buf, 2, d);
     constexpr int kBatch = 8;   // issue a batch of loads before using any
     for (int j0 = threadIdx.x; j0 < L; j0 += kBatch * blockDim.x) {
         double2 u[kBatch], v[kBatch];
@@ -523,12 +631,17 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
 #pragma unroll
         for (int i = 0; i < kBatch; ++i)
             if (j0 + i * blockDim.x < L) {
+                if (d.blue) {
+                    const double2 c = chirp[j0 + i * blockDim.x];
+                    u[i] = cmul(u[i], c);
+                    v[i] = cmul(v[i], c);
+                }
                 buf[p[i]] = u[i];
-                buf[L + p[i]] = v[i];
+                buf[Lb + p[i]] = v[i];
             }
     }
     __syncthreads();
-    dft_passes(buf, 2, d, Wt, W + L, false);
+    row_dft<true>(buf, 2, d, Wt, W + Lb, H, false);
     const double w = weights[n + r];
     const double invL = 1.0 / (double)L;
     const int mtop = 2 * n - 1;
@@ -564,15 +677,26 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
             const int am = a0 + i * blockDim.x;
             if (am >= nord) continue;
             const int bn = L - am;
-            double2 sa = buf[am], sb = buf[L + am];
+            const int pa = d.blue ? perm[am] : am, pb = d.blue ? perm[bn] : bn;
+            double2 sa = buf[pa], sb = buf[Lb + pa];
+            if (d.blue) {
+                const double2 c = chirp[am];
+                sa = cmul(sa, c);
+                sb = cmul(sb, c);
+            }
             const double2 cp = make_double2(tp[i].x, -tp[i].y);
             sa = cmul(make_double2(sa.x * invL, sa.y * invL), cp);
             sb = cmul(make_double2(sb.x * invL, sb.y * invL), cp);
             double2 na = make_double2(0.0, 0.0), nb = na;
             if (am > 0) {
                 const double2 cn = make_double2(tn[i].x, -tn[i].y);
-                na = buf[bn];
-                nb = buf[L + bn];
+                na = buf[pb];
+                nb = buf[Lb + pb];
+                if (d.blue) {
+                    const double2 c = chirp[bn];
+                    na = cmul(na, c);
+                    nb = cmul(nb, c);
+                }
                 na = cmul(make_double2(na.x * invL, na.y * invL), cn);
                 nb = cmul(make_double2(nb.x * invL, nb.y * invL), cn);
             }
@@ -702,15 +826,55 @@ __global__ void orders_fold_kernel(int n, const bf_half *__restrict__ halves,
 }
 
 std::vector<int> factorize(int64_t L) {
+    // prime factors ascending, with pairs of 2s merged into the radix-4 pass
     std::vector<int> f;
-    // prefer the templated radices; 4 only where two 2s pair up
-    for (int p = 2; (int64_t)p * p <= L; ++p)
+    int twos = 0;
+    while (L % 2 == 0) {
+        ++twos;
+        L /= 2;
+    }
+    for (; twos >= 2; twos -= 2) f.push_back(4);
+    if (twos) f.push_back(2);
+    for (int p = 3; (int64_t)p * p <= L; p += 2)
         while (L % p == 0) {
             f.push_back(p);
             L /= p;
         }
     if (L > 1) f.push_back((int)L);
     return f;
+}
+
+// Smallest 2-3-5-7-smooth length >= need (Bluestein convolution length).
+int64_t smooth_at_least(int64_t need) {
+    int64_t best = INT64_MAX;
+    for (int64_t a = 1; a < 2 * need; a *= 2)
+        for (int64_t b = a; b < 2 * need; b *= 3)
+            for (int64_t c = b; c < 2 * need; c *= 5)
+                for (int64_t d = c; d < 2 * need; d *= 7)
+                    if (d >= need && d < best) best = d;
+    return best;
+}
+
+// Host FFT in long double (recursive, smallest prime first), sign -1 or +1:
+// the Bluestein kernel spectrum H, computed once per length.
+void host_fft(std::vector<std::complex<long double>> &a, int sign) {
+    const int64_t n = (int64_t)a.size();
+    if (n <= 1) return;
+    int64_t p = 2;
+    while (n % p) ++p;
+    const int64_t m = n / p;
+    std::vector<std::vector<std::complex<long double>>> sub(p, std::vector<std::complex<long double>>(m));
+    for (int64_t i = 0; i < n; ++i) sub[i % p][i / p] = a[i];
+    for (auto &v : sub) host_fft(v, sign);
+    const long double two_pi = 6.283185307179586476925286766559L;
+    for (int64_t k = 0; k < n; ++k) {
+        std::complex<long double> acc = 0;
+        for (int64_t r = 0; r < p; ++r) {
+            const long double ang = sign * two_pi * (long double)((r * k) % n) / (long double)n;
+            acc += sub[r][k % m] * std::complex<long double>(std::cos(ang), std::sin(ang));
+        }
+        a[k] = acc;
+    }
 }
 
 int perm_of(int64_t nidx, const std::vector<int> &rad, int upto) {
@@ -725,6 +889,8 @@ int perm_of(int64_t nidx, const std::vector<int> &rad, int upto) {
 DftDesc make_desc(const bfsht_plan *pl) {
     DftDesc d;
     d.L = (int)pl->dft_L;
+    d.Lb = (int)pl->dft_Lb;
+    d.blue = pl->dft_blue ? 1 : 0;
     d.nrad = (int)pl->dft_radix.size();
     int64_t span = 1;
     int tw = 0, ro = 0;
@@ -735,6 +901,7 @@ DftDesc make_desc(const bfsht_plan *pl) {
         d.span_inv[i] = span == 1 ? 0u : (unsigned)(((1ULL << 32) + span - 1) / span);
         d.tw_off[i] = tw;
         d.root_off[i] = ro;
+        d.span[i] = (int)span;
         tw += (int)((pl->dft_radix[i] - 1) * span);
         ro += pl->dft_radix[i];
         span *= pl->dft_radix[i];
@@ -763,9 +930,26 @@ int dft_anal_smem(int64_t L, int64_t nh, int gen) {
 
 }  // namespace
 
+// Tables of the length-L DFT stage (built once per length, on the plan's
+// device).  Lengths whose prime factors are all <= kGenMaxP run as direct
+// mixed-radix rows; any other length (a prime factor above 255, e.g. N=2048's
+// L = 8191 or N=66's L = 263 = prime) runs as a Bluestein row of the
+// smallest 2-3-5-7-smooth length M >= 2L-1.  BFSHT_BLUESTEIN_ABOVE=p moves
+// the threshold (tests force Bluestein onto small lengths with it).
 int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
-    if (pl->dft_L == L) return 0;
-    std::vector<int> rad = factorize(L);
+    int above = kGenMaxP;
+    if (const char *e = std::getenv("BFSHT_BLUESTEIN_ABOVE")) above = std::atoi(e);
+    std::vector<int> rad_l = factorize(L);
+    bool blue = false;
+    for (int p : rad_l)
+        if (p > above || p > kGenMaxP) blue = true;
+    if (pl->dft_L == L && pl->dft_blue == blue) return 0;
+    const int64_t Lb = blue ? smooth_at_least(2 * L - 1) : L;
+    if (Lb > (1 << 20)) {
+        bfsht_set_error("DFT length too large (buffer above 2^20)");
+        return -4;
+    }
+    std::vector<int> rad = blue ? factorize(Lb) : rad_l;
     if ((int)rad.size() > kMaxRadix) {
         bfsht_set_error("DFT length has too many prime factors");
         return -4;
@@ -777,7 +961,7 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         for (int p : rad) {
             if (span > 1) {
                 const uint64_t inv = ((1ULL << 32) + span - 1) / span;
-                for (int64_t x = 0; x < L; ++x)
+                for (int64_t x = 0; x < Lb; ++x)
                     if ((int64_t)(((uint64_t)x * inv) >> 32) != x / span) {
                         bfsht_set_error("DFT index division check failed");
                         return -4;
@@ -786,18 +970,13 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
             span *= p;
         }
     }
-    for (int p : rad)
-        if (p > kGenMaxP) {
-            bfsht_set_error("DFT length has a prime factor above 256 (needs Bluestein)");
-            return -4;
-        }
-    std::vector<double> w(2 * L), tw(2 * L), wt;
-    std::vector<int32_t> perm(L);
+    std::vector<double> w(2 * Lb), tw(2 * L), wt;
+    std::vector<int32_t> perm(Lb);
     const double two_pi = 6.283185307179586476925286766559;
-    for (int64_t k = 0; k < L; ++k) {
-        // exp(-2 pi i k / L), argument reduced to (-pi, pi] for accuracy
-        int64_t kk = k <= L / 2 ? k : k - L;
-        double a = -two_pi * (double)kk / (double)L;
+    for (int64_t k = 0; k < Lb; ++k) {
+        // exp(-2 pi i k / Lb), argument reduced to (-pi, pi] for accuracy
+        int64_t kk = k <= Lb / 2 ? k : k - Lb;
+        double a = -two_pi * (double)kk / (double)Lb;
         w[2 * k] = std::cos(a);
         w[2 * k + 1] = std::sin(a);
         perm[k] = perm_of(k, rad, (int)rad.size());
@@ -810,17 +989,17 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         tw[2 * b] = t.real();
         tw[2 * b + 1] = t.imag();
     }
-    // pass table: [0, L) inter-pass twiddles, pass after pass, entry
-    // (q-1)*span + k = w[q k L/(span P)]; then the radix roots of every
-    // pass, w[t L/P] for t < P (the same values the flat table held)
+    // pass table: [0, Lb) inter-pass twiddles, pass after pass, entry
+    // (q-1)*span + k = w[q k Lb/(span P)]; then the radix roots of every
+    // pass, w[t Lb/P] for t < P
     {
-        wt.assign(2 * L, 0.0);
+        wt.assign(2 * Lb, 0.0);
         int64_t span = 1, off = 0;
         for (int p : rad) {
-            const int64_t tstep = L / (span * p);
+            const int64_t tstep = Lb / (span * p);
             for (int q = 1; q < p; ++q)
                 for (int64_t k = 0; k < span; ++k) {
-                    const int64_t e = (q * k * tstep) % L;
+                    const int64_t e = (q * k * tstep) % Lb;
                     wt[2 * (off + (q - 1) * span + k)] = w[2 * e];
                     wt[2 * (off + (q - 1) * span + k) + 1] = w[2 * e + 1];
                 }
@@ -829,36 +1008,71 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
         }
         for (int p : rad)
             for (int t = 0; t < p; ++t) {
-                const int64_t e = t * (L / p);
+                const int64_t e = t * (Lb / p);
                 wt.push_back(w[2 * e]);
                 wt.push_back(w[2 * e + 1]);
             }
     }
+    // Bluestein: chirp c_j = exp(-i pi j^2 / L) (j^2 reduced mod 2L, exact
+    // in int64) and H = FFT_M(h) / M, h_d = conj(c_|d|) at d mod M, |d| < L
+    std::vector<double> chirp, hh;
+    if (blue) {
+        const long double pi = 3.14159265358979323846264338327950288L;
+        std::vector<std::complex<long double>> c(L), h(Lb, 0.0L);
+        for (int64_t j = 0; j < L; ++j) {
+            const int64_t r = (j * j) % (2 * L);
+            const long double ang = -pi * (long double)r / (long double)L;
+            c[j] = std::complex<long double>(std::cos(ang), std::sin(ang));
+        }
+        for (int64_t d = 0; d < L; ++d) {
+            h[d] = std::conj(c[d]);
+            if (d) h[Lb - d] = std::conj(c[d]);
+        }
+        host_fft(h, -1);
+        chirp.resize(2 * L);
+        hh.resize(2 * Lb);
+        for (int64_t j = 0; j < L; ++j) {
+            chirp[2 * j] = (double)c[j].real();
+            chirp[2 * j + 1] = (double)c[j].imag();
+        }
+        for (int64_t k = 0; k < Lb; ++k) {
+            hh[2 * k] = (double)(h[k].real() / (long double)Lb);
+            hh[2 * k + 1] = (double)(h[k].imag() / (long double)Lb);
+        }
+    }
     // re-prepare for a new length: every table and the scratch of the old one go
     for (void *p : {(void *)pl->dft_w, (void *)pl->dft_perm, (void *)pl->dft_tw,
-                    (void *)pl->dft_scratch})
+                    (void *)pl->dft_scratch, (void *)pl->dft_chirp, (void *)pl->dft_hhat})
         if (p) cudaFree(p);
-    pl->dft_w = pl->dft_tw = nullptr;
+    pl->dft_w = pl->dft_tw = pl->dft_chirp = pl->dft_hhat = nullptr;
     pl->dft_perm = nullptr;
     pl->dft_scratch = nullptr;
     pl->dft_scratch_rows = 0;
     pl->dft_L = 0;
     BF_CUDA(cudaMalloc(&pl->dft_w, 8 * wt.size()));
     BF_CUDA(cudaMalloc(&pl->dft_tw, 16 * L));
-    BF_CUDA(cudaMalloc(&pl->dft_perm, 4 * L));
+    BF_CUDA(cudaMalloc(&pl->dft_perm, 4 * Lb));
     BF_CUDA(cudaMemcpy(pl->dft_w, wt.data(), 8 * wt.size(), cudaMemcpyHostToDevice));
     BF_CUDA(cudaMemcpy(pl->dft_tw, tw.data(), 16 * L, cudaMemcpyHostToDevice));
-    BF_CUDA(cudaMemcpy(pl->dft_perm, perm.data(), 4 * L, cudaMemcpyHostToDevice));
+    BF_CUDA(cudaMemcpy(pl->dft_perm, perm.data(), 4 * Lb, cudaMemcpyHostToDevice));
+    if (blue) {
+        BF_CUDA(cudaMalloc(&pl->dft_chirp, 16 * L));
+        BF_CUDA(cudaMalloc(&pl->dft_hhat, 16 * Lb));
+        BF_CUDA(cudaMemcpy(pl->dft_chirp, chirp.data(), 16 * L, cudaMemcpyHostToDevice));
+        BF_CUDA(cudaMemcpy(pl->dft_hhat, hh.data(), 16 * Lb, cudaMemcpyHostToDevice));
+    }
     pl->dft_radix = rad;
     pl->dft_L = L;
+    pl->dft_Lb = Lb;
+    pl->dft_blue = blue;
     pl->dft_gen = dft_gen_bytes(rad);
     const int gen = pl->dft_gen;
-    const int need = dft_smem_bytes(L, 2);
+    const int need = dft_smem_bytes(Lb, 2);
     int maxsm = 0;
     BF_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
     if (need + gen > maxsm) {
         const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
-        BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * L * rows));
+        BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * Lb * rows));
         pl->dft_scratch_rows = rows;
     }
     // dynamic shared-memory limits are raised per launch (bf_ensure_smem)
@@ -884,15 +1098,15 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
         auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
         int rc_ = bf_ensure_smem((const void *)kern_, smem_);
         if (rc_) return rc_;
         kern_<<<nblk, kDftThreads, smem_, st>>>(
         d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), pl->info[10],
-        2 * pl->norders, BF_NRHS);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), pl->info[10],
+        2 * pl->norders, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
     }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -908,17 +1122,17 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const DftDesc d = make_desc(pl);
     const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     const int64_t nh = 2 * (int64_t)pl->norders;
-    const bool ysm = sm && dft_y_smem(pl->dft_L, nh, pl->dft_gen);
+    const bool ysm = sm && dft_y_smem(pl->dft_Lb, nh, pl->dft_gen);
     {
-        const int smem_ = sm ? (ysm ? dft_anal_smem(pl->dft_L, nh, pl->dft_gen) : dft_pair_smem(pl->dft_L, pl->dft_gen)) : pl->dft_gen;
+        const int smem_ = sm ? (ysm ? dft_anal_smem(pl->dft_Lb, nh, pl->dft_gen) : dft_pair_smem(pl->dft_Lb, pl->dft_gen)) : pl->dft_gen;
         auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
         int rc_ = bf_ensure_smem((const void *)kern_, smem_);
         if (rc_) return rc_;
         kern_<<<nblk, kDftThreads, smem_, st>>>(
         d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen),
-        ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS);
+        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen),
+        ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
     }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -1154,7 +1368,7 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<double2 *>(out) + b * ngrid, sm,
                 reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen), pl->info[10],
-                2 * pl->norders, ew);
+                2 * pl->norders, ew, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
             }
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
@@ -1174,7 +1388,7 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
                 reinterpret_cast<const double2 *>(pl->dft_w),
                 reinterpret_cast<const double2 *>(in) + b * ngrid, weights, 0, n, sm,
                 reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen),
-                ysm ? pl->node_y : nullptr, (int)nh, ew);
+                ysm ? pl->node_y : nullptr, (int)nh, ew, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
             }
             BF_CUDA(cudaGetLastError());
             pl->launches += 1;
@@ -1195,7 +1409,7 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
                 cudaStream_t st) {
     int rc = bf_dft_prepare(pl, L);
     if (rc) return rc;
-    const bool sm = dft_smem_bytes(L, 1) + pl->dft_gen <= 227 * 1024 && pl->dft_scratch == nullptr;
+    const bool sm = dft_smem_bytes(pl->dft_Lb, 1) + pl->dft_gen <= 227 * 1024 && pl->dft_scratch == nullptr;
     int grid = (int)(rows < 4096 ? rows : 4096);
     if (!sm) grid = (int)std::min<int64_t>(grid, pl->dft_scratch_rows);
     if (grid <= 0) return 0;
@@ -1203,13 +1417,13 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
     // footprint (2 CTAs per SM) for the all-templated lengths
     auto kern = sm ? (pl->dft_gen ? dft_rows_kernel<true, true> : dft_rows_kernel<true, false>)
                    : (pl->dft_gen ? dft_rows_kernel<false, true> : dft_rows_kernel<false, false>);
-    const int smem = sm ? dft_smem_bytes(L, 1) + pl->dft_gen : pl->dft_gen;
+    const int smem = sm ? dft_smem_bytes(pl->dft_Lb, 1) + pl->dft_gen : pl->dft_gen;
     rc = bf_ensure_smem((const void *)kern, smem);
     if (rc) return rc;
     kern<<<grid, kDftThreads, smem, st>>>(
         make_desc(pl), reinterpret_cast<const double2 *>(in), reinterpret_cast<double2 *>(out), rows,
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w), dir == BFSHT_INVERSE, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch));
+        reinterpret_cast<double2 *>(pl->dft_scratch), reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
@@ -1224,7 +1438,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
     {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
         auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
         int rc_ = bf_ensure_smem((const void *)kern_, smem_);
         if (rc_) return rc_;
@@ -1232,7 +1446,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
         make_desc(pl), n, halves, ybuf, r_begin, r_count,
         reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
         reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), (int64_t)0, 0, BF_NRHS);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), (int64_t)0, 0, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
     }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -1248,7 +1462,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     const bool sm = pl->dft_scratch == nullptr;
     const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
     {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_L, pl->dft_gen) : pl->dft_gen;
+        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
         auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
         int rc_ = bf_ensure_smem((const void *)kern_, smem_);
         if (rc_) return rc_;
@@ -1256,7 +1470,7 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
         make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
         pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
         reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_L, pl->dft_gen), nullptr, 0, BF_NRHS);
+        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), nullptr, 0, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
     }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
