@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (order-sharded, NCCL) runner even at one "
                          "rank: exercises the scaling path of this script on one GPU")
+    ap.add_argument("--plan-cache", default="",
+                    help="directory of packed per-rank plans (BFPK files): loaded when "
+                         "present, written otherwise (skips planning on later runs)")
     ap.add_argument("--regen", type=float, default=0.0,
                     help="fraction of full-height dense turning tiles regenerated "
                          "on the GPU from recurrence seeds (SURVEY f1)")
@@ -334,10 +337,39 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
     sharded = world > 1 or args.force_sharded
     if sharded and args.batch > 1:
         raise SystemExit("--batch > 1 is single-GPU only")
+    n = args.n
+    params = SamplingConfig(tolerance=args.tol)
+    procs = args.plan_procs or max(1, (os.cpu_count() or 1) // world)
+    orders = D.lpt_orders(n, world)[rank] if sharded else list(range(2 * n))
+    # the CPU baseline / oracle check (rank 0 at N=1) need the host plans
+    need_plans = rank == 0 and world == 1 and not args.no_cpu_baseline
+
+    # planning first, before CUDA / NCCL start threads in this process; a
+    # packed-plan cache (--plan-cache) skips planning and packing
+    t0 = time.time()
+    plans, packed, cache_hit = None, None, False
+    cache = None
+    if args.plan_cache:
+        from paper_2004_11346_b200.pack import load_packed, pack_plans, save_packed
+        os.makedirs(args.plan_cache, exist_ok=True)
+        cache = os.path.join(args.plan_cache,
+                             f"bfsht_n{n}_tol{args.tol:g}_w{world if sharded else 0}_r{rank}"
+                             f"_regen{args.regen:g}.bfpk")
+        if os.path.exists(cache):
+            packed, cache_hit = load_packed(cache), True
+    if packed is None or need_plans:
+        plans = plan_orders(n, orders, params, processes=procs)
+    if cache and not cache_hit:
+        packed = pack_plans(plans, regen=args.regen)
+        save_packed(packed, cache)
+    t_plan = time.time() - t0
+    from paper_2004_11346_b200.legendre import gauss_legendre
+    weights = gauss_legendre(2 * n).weights
+
+    torch.cuda.set_device(local)
     if sharded:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if world == 1:
@@ -345,27 +377,17 @@ def run_ours(args):
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = args.n
-    params = SamplingConfig(tolerance=args.tol)
-    procs = args.plan_procs or max(1, (os.cpu_count() or 1) // world)
-
-    t0 = time.time()
-    if not sharded:
-        orders = list(range(2 * n))
-    else:
-        orders = D.lpt_orders(n, world)[rank]
-    plans = plan_orders(n, orders, params, processes=procs)
-    t_plan = time.time() - t0
-    payload_values = sum(p.stats["total_nnz"] for p in plans)
 
     t0 = time.time()
     if not sharded:
         eng = ShtDevice.__new__(ShtDevice)
         eng.n = n
-        eng.plan = DevicePlan(plans, weights=plans[0].quadrature.weights, regen=args.regen)
+        eng.plan = DevicePlan(plans or [], weights=weights, regen=args.regen, packed=packed)
         runner = D.SingleRunner(eng, batch=args.batch)
     else:
-        runner = D.ShardedSht(n, plans, orders, rank, world, regen=args.regen)
+        runner = D.ShardedSht(n, plans or [], orders, rank, world, regen=args.regen,
+                              packed=packed, weights=weights)
+    payload_values = runner.dp.packed.stats["payload_values"]
     torch.cuda.synchronize()
     t_up = time.time() - t0
 
@@ -496,7 +518,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
             "roundtrip_rel_l2": rt,
-            "setup_s": {"plan": t_plan, "pack_upload": t_up},
+            "setup_s": {"plan": t_plan, "pack_upload": t_up,
+                        "plan_cache": ("hit" if cache_hit else "written") if cache else None},
         }
         if check is not None:
             line["check_vs_oracle"] = check

@@ -226,6 +226,49 @@ int bfsht_anal_rows(bfsht_plan *pl, const void *halves, double *ubuf,
                     int64_t r_begin, int64_t r_count, const double *grid,
                     const double *weights, void *stream);
 
+/* ------------------------------------------------ NCCL communicator + the
+ * exchange (SURVEY 8(b) "bfsht_comm_init + bfsht_alltoall_transpose").
+ * NCCL is loaded at run time (libnccl.so.2; the copy already in the process
+ * if there is one).  One rank per GPU; call on the rank's current device. */
+typedef struct bfsht_comm bfsht_comm;
+#define BFSHT_COMM_ID_BYTES 128        /* = NCCL_UNIQUE_ID_BYTES */
+/* Rank 0 creates the id (ncclGetUniqueId) and ships it to the other ranks
+ * out of band (MPI, a TCP store, torch.distributed, ...). */
+int bfsht_comm_unique_id(void *id);
+int bfsht_comm_init(const void *id, int rank, int nranks, bfsht_comm **out);
+void bfsht_comm_free(bfsht_comm *c);
+/* Grouped ncclSend / ncclRecv: peer q gets send_counts[q] entries of
+ * entry_doubles fp64 each (peers' runs back to back in send), and
+ * recv_counts[q] entries from peer q land back to back in recv. */
+int bfsht_alltoall_transpose(bfsht_comm *c, const double *send, const int64_t *send_counts,
+                             double *recv, const int64_t *recv_counts, int64_t entry_doubles,
+                             void *stream);
+
+/* Host-only (no GPU needed): the orders of `rank` under the greedy LPT
+ * split of m = 0..2N-1 on the cost 2N-m (orders: capacity 2N, may be NULL
+ * to count), and the exchange layout of that rank: recv_layout = 4N
+ * bf_half-like records {x, y, ncols, m} (entry (m, parity, r) of the
+ * theta-major receive buffer at y + (r - r0) * x), send / recv entry counts
+ * per peer (row pairs split contiguously: peer q owns [qN/P, (q+1)N/P)). */
+int bfsht_shard_orders(int n, int nranks, int rank, int32_t *orders, int32_t *count);
+int bfsht_exchange_layout(int n, int nranks, int rank, void *recv_layout, int64_t *send_counts,
+                          int64_t *recv_counts);
+
+/* The whole order-sharded SHT of one rank.  `pl` must hold exactly the
+ * orders bfsht_shard_orders gives this rank (ascending); coefficients are
+ * the shard layout (bfsht_shard_pack); the grid is this rank's 2*rc rows
+ * (rows n-r0-rc .. n-r0-1, then n+r0 .. n+r0+rc-1).  Forward = shard pack,
+ * ALT, all-to-all of the node halves (sent straight from the row-major Yr
+ * array), fused synthesis/DFT of the rank's row pairs; inverse the reverse.
+ * info: 0 r0, 1 rc, 2 shard coefficient count, 3 receive-buffer entries. */
+typedef struct bfsht_sharded bfsht_sharded;
+int bfsht_sharded_create(bfsht_plan *pl, bfsht_comm *comm, bfsht_sharded **out);
+int64_t bfsht_sharded_info(const bfsht_sharded *s, int64_t info[4]);
+int bfsht_sharded_forward(bfsht_sharded *s, const double *coeffs, double *grid, void *stream);
+int bfsht_sharded_inverse(bfsht_sharded *s, const double *grid, double *coeffs,
+                          const double *weights, void *stream);
+void bfsht_sharded_free(bfsht_sharded *s);
+
 #ifdef __cplusplus
 }
 #endif

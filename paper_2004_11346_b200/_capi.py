@@ -55,6 +55,28 @@ def declare(lib):
     lib.bfsht_synth_rows.argtypes = [_P, _P, _P, _I64, _I64, _P, _P]
     lib.bfsht_anal_rows.restype = _I
     lib.bfsht_anal_rows.argtypes = [_P, _P, _P, _I64, _I64, _P, _P, _P]
+    lib.bfsht_comm_unique_id.restype = _I
+    lib.bfsht_comm_unique_id.argtypes = [_P]
+    lib.bfsht_comm_init.restype = _I
+    lib.bfsht_comm_init.argtypes = [_P, _I, _I, ctypes.POINTER(_P)]
+    lib.bfsht_comm_free.restype = None
+    lib.bfsht_comm_free.argtypes = [_P]
+    lib.bfsht_alltoall_transpose.restype = _I
+    lib.bfsht_alltoall_transpose.argtypes = [_P, _P, _P, _P, _P, _I64, _P]
+    lib.bfsht_shard_orders.restype = _I
+    lib.bfsht_shard_orders.argtypes = [_I, _I, _I, _P, _P]
+    lib.bfsht_exchange_layout.restype = _I
+    lib.bfsht_exchange_layout.argtypes = [_I, _I, _I, _P, _P, _P]
+    lib.bfsht_sharded_create.restype = _I
+    lib.bfsht_sharded_create.argtypes = [_P, _P, ctypes.POINTER(_P)]
+    lib.bfsht_sharded_info.restype = _I64
+    lib.bfsht_sharded_info.argtypes = [_P, _P]
+    lib.bfsht_sharded_forward.restype = _I
+    lib.bfsht_sharded_forward.argtypes = [_P, _P, _P, _P]
+    lib.bfsht_sharded_inverse.restype = _I
+    lib.bfsht_sharded_inverse.argtypes = [_P, _P, _P, _P, _P]
+    lib.bfsht_sharded_free.restype = None
+    lib.bfsht_sharded_free.argtypes = [_P]
 
 
 # every symbol include/bfsht_b200.h declares (checked by tests on CPU)
@@ -67,7 +89,10 @@ EXPORTS = (
     "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
     "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",
     "bfsht_gather_entries", "bfsht_scatter_entries", "bfsht_synth_rows",
-    "bfsht_anal_rows",
+    "bfsht_anal_rows", "bfsht_comm_unique_id", "bfsht_comm_init", "bfsht_comm_free",
+    "bfsht_alltoall_transpose", "bfsht_shard_orders", "bfsht_exchange_layout",
+    "bfsht_sharded_create", "bfsht_sharded_info", "bfsht_sharded_forward",
+    "bfsht_sharded_inverse", "bfsht_sharded_free",
 )
 
 

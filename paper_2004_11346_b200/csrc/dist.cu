@@ -82,30 +82,38 @@ int grid_for(int64_t count) {
 
 }  // namespace
 
-extern "C" {
-
-int bfsht_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs, void *stream) {
-    DeviceGuard guard(pl);
-    if (!pl) return -1;
+int bf_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs, cudaStream_t st) {
     if (pl->norders == 0) return 0;
     dim3 g((pl->n + 255) / 256, pl->norders);
-    shard_pack_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(
-        pl->n, pl->halves, off, reinterpret_cast<const double2 *>(coeffs), pl->arena);
+    shard_pack_kernel<<<g, 256, 0, st>>>(pl->n, pl->halves, off,
+                                         reinterpret_cast<const double2 *>(coeffs), pl->arena);
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
 }
 
-int bfsht_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs, void *stream) {
-    DeviceGuard guard(pl);
-    if (!pl) return -1;
+int bf_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs, cudaStream_t st) {
     if (pl->norders == 0) return 0;
     dim3 g((pl->n + 255) / 256, pl->norders);
-    shard_unpack_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(
-        pl->n, pl->halves, off, pl->arena, reinterpret_cast<double2 *>(coeffs));
+    shard_unpack_kernel<<<g, 256, 0, st>>>(pl->n, pl->halves, off, pl->arena,
+                                           reinterpret_cast<double2 *>(coeffs));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;
+}
+
+extern "C" {
+
+int bfsht_shard_pack(bfsht_plan *pl, const int64_t *off, const double *coeffs, void *stream) {
+    DeviceGuard guard(pl);
+    if (!pl) return -1;
+    return bf_shard_pack(pl, off, coeffs, (cudaStream_t)stream);
+}
+
+int bfsht_shard_unpack(bfsht_plan *pl, const int64_t *off, double *coeffs, void *stream) {
+    DeviceGuard guard(pl);
+    if (!pl) return -1;
+    return bf_shard_unpack(pl, off, coeffs, (cudaStream_t)stream);
 }
 
 int bfsht_gather_entries(bfsht_plan *pl, const int32_t *idx, int64_t count, double *out,

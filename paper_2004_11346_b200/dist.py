@@ -7,9 +7,14 @@ per-order cost proxy 2N-|m|).  The phi DFT needs every order of a
 colatitude row (sht.py:148,161), so each direction has exactly one exchange:
 an NCCL all-to-all that transposes node-half entries between the m-major
 ALT layout (owner of m) and the theta-major DFT layout (owner of row pairs
-r, n+r / n-1-r).  Entries are moved with gather/scatter kernels into
-contiguous per-destination chunks, so the collective is a single
-``all_to_all_single`` per direction.
+r, n+r / n-1-r).  The forward sends straight from the row-major node array
+(each peer's rows are one contiguous run); the inverse sends them back and
+one kernel moves each entry to its m-major node half.
+
+The exchange runs in the C ABI (csrc/comm.cu: bfsht_comm_init,
+bfsht_alltoall_transpose, bfsht_sharded_forward / _inverse) over its own
+NCCL communicator; torch.distributed only carries the NCCL unique id and
+the max-over-ranks timing.
 
 Both runners expose the same interface to bench.py / smoke():
 forward(coeffs, grid), inverse(grid, coeffs), time_alt, time_e2e, ...
@@ -19,7 +24,7 @@ import ctypes
 import numpy as np
 
 from ._capi import check
-from .pack import HALF_DTYPE, NRHS
+from .pack import HALF_DTYPE
 
 FORWARD, INVERSE = 0, 1
 
@@ -45,25 +50,28 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
-def _stream(torch):
-    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(torch, device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 class ExchangePlan:
-    """Host-side layout of the per-direction all-to-all (no device code).
+    """Host view of one rank's exchange (the layout the C ABI computes,
+    bfsht_exchange_layout in csrc/comm.cu; no device code).
 
-    Chunks are row-major: the chunk for destination q holds, for each of
-    q's row pairs r (ascending), the 2 x len(orders) entries (order, parity)
-    of this rank — exactly one contiguous run of the forward node array
-    Yr[r][order][parity] per row (``send_idx``, a gather list).  For the
-    inverse the same positions map back to the m-major node halves the
-    inverse ALT reads (``scatter_idx``, -1 for absent halves).  On the
-    receive side the chunk from source s lands so that entry (m, parity, r)
-    sits at recv_layout[2m+parity].y + (r - r0) * recv_layout[2m+parity].x:
-    the addressing the DFT kernels take.
+    Forward: the entries for peer q are this rank's Yr rows [a_q, b_q) —
+    one contiguous run of the row-major node array Yr[r][order][parity]
+    (arena entries yr + r * w + h, w = 2 x len(orders)) — sent back to back
+    in peer order (send_counts).  The receiver keeps the sources' runs back
+    to back: entry (m, parity, r) sits at recv_layout[2m+parity].y +
+    (r - r0) * recv_layout[2m+parity].x, the addressing the DFT kernels
+    take.  Inverse: the same runs travel back into the Yr region, and entry
+    yr + r * w + h moves to the m-major node half halves[h].y + r that the
+    inverse ALT reads (yr_to_halves).
     """
 
     def __init__(self, n, world, rank, halves, yr):
+        from . import native
+        lib = native.cuda()
         self.n, self.world, self.rank = n, world, rank
         self.all_orders = lpt_orders(n, world)
         self.orders = self.all_orders[rank]
@@ -74,37 +82,30 @@ class ExchangePlan:
         if len(h) != 2 * len(self.orders) or \
                 list(h["m"][0::2]) != list(self.orders):
             raise ValueError("halves do not match this rank's orders")
-        w = 2 * len(self.orders)
-        ys = np.where(h["ncols"] > 0, h["y"], -1).astype(np.int64)
-        gather, scatter, self.send_counts = [], [], []
-        for a, b in self.rows:
-            r = np.arange(a, b, dtype=np.int64)[:, None]
-            gather.append((yr + r * w + np.arange(w)[None, :]).ravel())
-            scatter.append(np.where(ys[None, :] >= 0, ys[None, :] + r, -1).ravel())
-            self.send_counts.append((b - a) * w)
-        self.send_idx = np.concatenate(gather).astype(np.int32)
-        self.scatter_idx = np.concatenate(scatter).astype(np.int32)
+        self.yr, self.w = int(yr), 2 * len(self.orders)
+        self.halves = h
         self.recv_layout = np.zeros(4 * n, dtype=HALF_DTYPE)
-        self.recv_counts = []
-        pos = 0
-        for s in range(world):
-            ws = 2 * len(self.all_orders[s])
-            for i, m in enumerate(self.all_orders[s]):
-                for par in range(2):
-                    hf = self.recv_layout[2 * m + par]
-                    hf["m"] = m
-                    hf["ncols"] = half_cols(n, m, par)
-                    hf["x"] = ws
-                    hf["y"] = pos + 2 * i + par
-            self.recv_counts.append(self.rc * ws)
-            pos += self.rc * ws
-        self.recv_entries = pos
+        sc = np.zeros(world, dtype=np.int64)
+        rcnt = np.zeros(world, dtype=np.int64)
+        check(lib, lib.bfsht_exchange_layout(n, world, rank, self.recv_layout.ctypes.data,
+                                             sc.ctypes.data, rcnt.ctypes.data),
+              "bfsht_exchange_layout")
+        self.send_counts = [int(v) for v in sc]
+        self.recv_counts = [int(v) for v in rcnt]
+        self.recv_entries = int(rcnt.sum())
         offs, at = [], 0
         for m in self.orders:
             offs.append(at)
             at += (2 * n - m) * (2 if m else 1)
         self.coeff_offsets = np.array(offs + [at], dtype=np.int64)
         self.coeff_len = at
+
+    def yr_to_halves(self):
+        """For every Yr entry (row-major, r then h) of this rank: the arena
+        entry of its m-major node half (-1 for an absent half)."""
+        ys = np.where(self.halves["ncols"] > 0, self.halves["y"], -1).astype(np.int64)
+        r = np.arange(self.n, dtype=np.int64)[:, None]
+        return np.where(ys[None, :] >= 0, ys[None, :] + r, -1).ravel()
 
 
 def half_cols(n, m, par):
@@ -283,43 +284,76 @@ class SingleRunner(_Common):
         return float(torch.linalg.norm(back - coeffs) / torch.linalg.norm(coeffs))
 
 class ShardedSht(_Common):
-    """Orders sharded over ranks, one NCCL all-to-all per direction.
+    """Orders sharded over ranks, one NCCL exchange per direction — the
+    native sharded transform of the C ABI (bfsht_sharded_forward /
+    _inverse, csrc/comm.cu): its own NCCL communicator (bfsht_comm_init;
+    torch.distributed only ships the unique id), grouped ncclSend/ncclRecv
+    straight from the row-major node array.
 
     Data layout per rank: coefficients of its own orders (shard layout, see
     bfsht_shard_pack), and grid rows of its row pairs
     [r0, r1): rows n-r1..n-r0-1 then n+r0..n+r1-1.
     """
 
-    def __init__(self, n, plans, orders, rank, world, group=None, regen=0.0):
+    def __init__(self, n, plans, orders, rank, world, group=None, regen=0.0, packed=None,
+                 weights=None):
         import torch
         import torch.distributed as dist
         from .api import DevicePlan
+        from .legendre import gauss_legendre
         self.torch, self.dist = torch, dist
         self.n, self.rank, self.world = n, rank, world
         self.group = group
         self.orders = list(orders)
-        self.dp = DevicePlan(plans, weights=plans[0].quadrature.weights
-                             if plans else None, regen=regen)
+        if weights is None:
+            weights = plans[0].quadrature.weights if plans else gauss_legendre(2 * n).weights
+        self.dp = DevicePlan(plans, weights=weights, regen=regen, packed=packed)
         lib = self.dp.lib
         self.lib = lib
-        dev = self.dp.device
         xp = ExchangePlan(n, world, rank, self.dp.packed.halves,
                           int(self.dp.packed.info[10]))
         self.xp = xp
         self.all_orders, self.rows = xp.all_orders, xp.rows
         self.r0, self.rc = xp.r0, xp.rc
-        self.send_idx = torch.from_numpy(xp.send_idx).to(dev)
-        self.scatter_idx = torch.from_numpy(xp.scatter_idx).to(dev)
         self.send_counts, self.recv_counts = xp.send_counts, xp.recv_counts
         self.recv_entries = xp.recv_entries
-        self.recv_layout = torch.from_numpy(xp.recv_layout.view(np.int32).copy()).to(dev)
-        self.sendbuf = torch.zeros((max(sum(xp.send_counts), 1), NRHS),
-                                   dtype=torch.float64, device=dev)
-        self.recvbuf = torch.zeros((max(xp.recv_entries, 1), NRHS),
-                                   dtype=torch.float64, device=dev)
         self.coeff_len = xp.coeff_len
-        self.coeff_off = torch.from_numpy(xp.coeff_offsets).to(dev)
         self.weights = self.dp.weights
+        # NCCL communicator of the C ABI: rank 0's unique id travels over
+        # the torch process group, nothing else does
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(lib, lib.bfsht_comm_unique_id(uid), "bfsht_comm_unique_id")
+        box = [uid.raw]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0, group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        self.comm = ctypes.c_void_p()
+        with torch.cuda.device(self.dp.device):
+            check(lib, lib.bfsht_comm_init(uid, rank, world, ctypes.byref(self.comm)),
+                  "bfsht_comm_init")
+            self.handle = ctypes.c_void_p()
+            check(lib, lib.bfsht_sharded_create(self.dp.handle, self.comm,
+                                                ctypes.byref(self.handle)),
+                  "bfsht_sharded_create")
+        info = (ctypes.c_int64 * 4)()
+        lib.bfsht_sharded_info(self.handle, info)
+        if (info[0], info[1], info[2], info[3]) != (xp.r0, xp.rc, xp.coeff_len, xp.recv_entries):
+            raise RuntimeError("native and host exchange layouts disagree")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.bfsht_sharded_free(self.handle)
+            self.handle = None
+        if getattr(self, "comm", None):
+            self.lib.bfsht_comm_free(self.comm)
+            self.comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def make_buffers(self, flat):
         torch = self.torch
@@ -329,35 +363,16 @@ class ShardedSht(_Common):
         return c, g, torch.empty_like(c)
 
     # --------------------------------------------------------- transforms
-    def _a2a(self, out, inp, out_counts, in_counts):
-        self.dist.all_to_all_single(out.view(-1), inp.view(-1),
-                                    [c * NRHS for c in out_counts],
-                                    [c * NRHS for c in in_counts], group=self.group)
-
     def forward(self, coeffs, grid):
-        lib, dp, st = self.lib, self.dp, _stream(self.torch)
-        check(lib, lib.bfsht_shard_pack(dp.handle, _ptr(self.coeff_off), _ptr(coeffs), st),
-              "bfsht_shard_pack")
-        dp.alt_apply(FORWARD)
-        check(lib, lib.bfsht_gather_entries(dp.handle, _ptr(self.send_idx),
-                                            self.send_idx.numel(), _ptr(self.sendbuf), st),
-              "bfsht_gather_entries")
-        self._a2a(self.recvbuf, self.sendbuf, self.recv_counts, self.send_counts)
-        check(lib, lib.bfsht_synth_rows(dp.handle, _ptr(self.recv_layout), _ptr(self.recvbuf),
-                                        self.r0, self.rc, _ptr(grid), st), "bfsht_synth_rows")
+        st = _stream(self.torch, self.dp.device)
+        check(self.lib, self.lib.bfsht_sharded_forward(self.handle, _ptr(coeffs), _ptr(grid), st),
+              "bfsht_sharded_forward")
 
     def inverse(self, grid, coeffs):
-        lib, dp, st = self.lib, self.dp, _stream(self.torch)
-        check(lib, lib.bfsht_anal_rows(dp.handle, _ptr(self.recv_layout), _ptr(self.recvbuf),
-                                       self.r0, self.rc, _ptr(grid), _ptr(self.weights), st),
-              "bfsht_anal_rows")
-        self._a2a(self.sendbuf, self.recvbuf, self.send_counts, self.recv_counts)
-        check(lib, lib.bfsht_scatter_entries(dp.handle, _ptr(self.scatter_idx),
-                                             self.scatter_idx.numel(), _ptr(self.sendbuf), st),
-              "bfsht_scatter_entries")
-        dp.alt_apply(INVERSE)
-        check(lib, lib.bfsht_shard_unpack(dp.handle, _ptr(self.coeff_off), _ptr(coeffs), st),
-              "bfsht_shard_unpack")
+        st = _stream(self.torch, self.dp.device)
+        check(self.lib, self.lib.bfsht_sharded_inverse(self.handle, _ptr(grid), _ptr(coeffs),
+                                                       _ptr(self.weights), st),
+              "bfsht_sharded_inverse")
 
     def shard_coeffs(self, flat):
         """This rank's coefficient shard from the full flat layout."""

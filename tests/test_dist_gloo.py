@@ -2,10 +2,15 @@
 
 Each rank plans and packs only its LPT share of the orders, runs the ALT
 through the numpy interpreter of the packed format (packed_emulator), and
-exchanges node-half entries with a real all_to_all_single using the
-ExchangePlan layout the GPU path uses (paper_2004_11346_b200/dist.py); the
-DFT stage is done in numpy on the rank's row pairs.  Results must match
-the CPU oracle's full transform on every rank's shard.
+exchanges node-half entries exactly as the native sharded transform does
+(csrc/comm.cu bfsht_sharded_forward / _inverse): the send buffer is the
+rank's row-major node array Yr itself (each peer's rows one contiguous
+run), the receive layout and per-peer counts come from the C ABI's host
+function bfsht_exchange_layout (through dist.ExchangePlan), and the inverse
+lands in the Yr region before the Yr -> m-major node-half move.  The
+transport is a gloo all_to_all_single with the same counts as the grouped
+ncclSend/ncclRecv.  The DFT stage is numpy on the rank's row pairs.  Results
+must match the CPU oracle's full transform on every rank's shard.
 """
 import os
 import socket
@@ -82,7 +87,9 @@ def _check_rank(rank, world):
                 arena[hf["x"]:hf["x"] + hf["ncols"]] = np.stack(
                     [a.real, a.imag, b.real, b.imag], 1)
     EMU.run_direction(pk, arena, 0)
-    send = torch.from_numpy(arena[xp.send_idx].copy())
+    yr, wy = xp.yr, xp.w
+    assert sum(xp.send_counts) == n * wy
+    send = torch.from_numpy(arena[yr:yr + n * wy].copy())   # Yr rows, peer after peer
     recv = torch.zeros((xp.recv_entries, 4), dtype=torch.float64)
     dist.all_to_all_single(recv.view(-1), send.view(-1),
                            [c * 4 for c in xp.recv_counts],
@@ -132,8 +139,10 @@ def _check_rank(rank, world):
                            [c * 4 for c in xp.send_counts],
                            [c * 4 for c in xp.recv_counts])
     arena[:] = 0.0
-    keep = xp.scatter_idx >= 0
-    arena[xp.scatter_idx[keep]] = back_send.numpy()[keep]
+    arena[yr:yr + n * wy] = back_send.numpy()       # back into the Yr region
+    dst = xp.yr_to_halves()                          # yr_to_halves_kernel
+    keep = dst >= 0
+    arena[dst[keep]] = arena[yr:yr + n * wy][keep]
     EMU.run_direction(pk, arena, 1)
     for o, m in enumerate(orders):
         for sign in ((1, -1) if m else (1,)):
@@ -164,6 +173,43 @@ def test_lpt_and_rows_cover():
         rows = row_split(n, world)
         assert rows[0][0] == 0 and rows[-1][1] == n
         assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+
+
+def test_native_lpt_and_layout_match_host():
+    # the C ABI's host-side shard / layout functions (used by the native
+    # sharded transform) against the Python restatement
+    import ctypes
+    from paper_2004_11346_b200 import native
+    from paper_2004_11346_b200.dist import half_cols, lpt_orders, row_split
+    from paper_2004_11346_b200.pack import HALF_DTYPE
+    lib = native.cuda()
+    for n, world in ((16, 2), (64, 3), (1024, 8), (4096, 8), (8, 1)):
+        parts = lpt_orders(n, world)
+        for rank in range(world):
+            buf = np.zeros(2 * n, dtype=np.int32)
+            cnt = ctypes.c_int32()
+            assert lib.bfsht_shard_orders(n, world, rank, buf.ctypes.data,
+                                          ctypes.addressof(cnt)) == 0
+            assert list(buf[:cnt.value]) == parts[rank]
+        rank = world - 1
+        lay = np.zeros(4 * n, dtype=HALF_DTYPE)
+        sc = np.zeros(world, dtype=np.int64)
+        rc = np.zeros(world, dtype=np.int64)
+        assert lib.bfsht_exchange_layout(n, world, rank, lay.ctypes.data, sc.ctypes.data,
+                                         rc.ctypes.data) == 0
+        rows = row_split(n, world)
+        w = 2 * len(parts[rank])
+        assert list(sc) == [(b - a) * w for a, b in rows]
+        mine = rows[rank][1] - rows[rank][0]
+        assert list(rc) == [mine * 2 * len(p) for p in parts]
+        pos = 0
+        for s_, p in enumerate(parts):
+            for i, m in enumerate(p):
+                for par in range(2):
+                    hf = lay[2 * m + par]
+                    assert (hf["m"], hf["ncols"], hf["x"], hf["y"]) == \
+                        (m, half_cols(n, m, par), 2 * len(p), pos + 2 * i + par)
+            pos += rc[s_]
 
 
 def test_exchange_plan_rejects_wrong_halves():
