@@ -24,7 +24,11 @@
 #include <complex>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "engine.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -720,6 +724,221 @@ __global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
     }
 }
 
+// ---- row-pair kernels on a 2-CTA cluster (rows that fit a CTA's half SM)
+//
+// The pair kernels above hold both rows n+r / n-1-r in one CTA (128 KB of
+// shared memory at N=1024 plus the twiddles), so one CTA of 8 warps runs
+// per SM and its load, transform and store phases serialize (ncu: 12%
+// occupancy, long-scoreboard stalls).  Here the pair is a thread-block
+// cluster of two CTAs, one row each (rank 0: row n+r, rank 1: row n-1-r),
+// 64 KB of shared memory and <= 128 registers per thread, so two clusters'
+// CTAs share an SM and one CTA's DRAM phase overlaps another's transform.
+// The parity coupling crosses the pair through distributed shared memory:
+// forward, each rank reads the node halves of half of the orders and
+// stores g_e + g_o into rank 0's row and g_e - g_o into rank 1's
+// (alt.py:225-236); inverse, after both row DFTs, each rank reads bins m
+// and L-m of both rows (one local, one remote) for half of the orders and
+// writes the weighted fold (alt.py:239-253).  Twiddle tables are read
+// through L1.  One cluster per row pair, grid = 2 * rows.
+template <bool GEN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
+    sht_synth_pair_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
+                          const double *__restrict__ arena, int r_count,
+                          const double2 *__restrict__ tw, const int *__restrict__ perm,
+                          const double2 *__restrict__ W, double2 *__restrict__ grid, int64_t yr,
+                          int ystride, int ew, const double2 *__restrict__ chirp,
+                          const double2 *__restrict__ H) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    extern __shared__ __align__(16) double2 dsm[];
+    const int L = d.L, Lb = d.Lb;
+    double2 *own = dsm;
+    double2 *peer = cl.map_shared_rank(dsm, rank ^ 1u);
+    double2 *bplus = rank ? peer : own, *bminus = rank ? own : peer;
+    const int rr = blockIdx.x >> 1;
+    if (d.blue)
+        for (int i = threadIdx.x; i < Lb; i += blockDim.x) own[i] = make_double2(0.0, 0.0);
+    cl.sync();   // both CTAs running (and Bluestein rows cleared) before remote stores
+    const int nord = 2 * n, half = (nord + 1) >> 1;
+    const int a_lo = rank ? half : 0, a_hi = rank ? nord : half;
+    constexpr int kBatch = 2;
+    for (int a0 = a_lo + threadIdx.x; a0 < a_hi; a0 += kBatch * blockDim.x) {
+        double2 op[kBatch], on[kBatch], ep[kBatch], en[kBatch], tp[kBatch], tn[kBatch];
+        int pp[kBatch], pn[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int am = a0 + i * blockDim.x;
+            const bool ok = am < a_hi;
+            op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
+            if (ok) {
+                const double2 *eo = nullptr, *ee = nullptr;
+                if (ystride > 0) {
+                    const double *rowp = arena + (yr + (int64_t)rr * ystride) * ew;
+                    eo = reinterpret_cast<const double2 *>(rowp + (2 * am) * ew);
+                    ee = reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew);
+                } else {
+                    const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
+                    if (ho.ncols > 0)
+                        eo = reinterpret_cast<const double2 *>(
+                            arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * ew);
+                    if (he.ncols > 0)
+                        ee = reinterpret_cast<const double2 *>(
+                            arena + ((int64_t)he.y + (int64_t)rr * he.x) * ew);
+                }
+                if (eo) {
+                    op[i] = eo[0];
+                    on[i] = eo[1];
+                }
+                if (ee) {
+                    ep[i] = ee[0];
+                    en[i] = ee[1];
+                }
+            }
+            const int bn = am > 0 && ok ? L - am : 0;
+            tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
+            tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+            if (d.blue && ok) {
+                tp[i] = cmul(tp[i], conjif(chirp[am], true));
+                tn[i] = cmul(tn[i], conjif(chirp[bn], true));
+            }
+            pp[i] = ok ? perm[am] : 0;
+            pn[i] = ok ? perm[bn] : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int am = a0 + i * blockDim.x;
+            if (am < a_hi) {
+                bplus[pp[i]] = cmul(make_double2(ep[i].x + op[i].x, ep[i].y + op[i].y), tp[i]);
+                bminus[pp[i]] = cmul(make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y), tp[i]);
+                if (am > 0) {
+                    bplus[pn[i]] = cmul(make_double2(en[i].x + on[i].x, en[i].y + on[i].y), tn[i]);
+                    bminus[pn[i]] = cmul(make_double2(en[i].x - on[i].x, en[i].y - on[i].y), tn[i]);
+                }
+            }
+        }
+    }
+    cl.sync();   // both rows assembled; no remote access after this point
+    row_dft<GEN>(own, 1, d, W, W + Lb, H, true);
+    double2 *out = grid + (int64_t)(rank ? r_count - 1 - rr : r_count + rr) * L;
+    for (int j0 = threadIdx.x; j0 < L; j0 += 2 * blockDim.x) {
+        double2 v[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < L) {
+                v[u] = own[d.blue ? perm[j] : j];
+                if (d.blue) v[u] = cmul(v[u], conjif(chirp[j], true));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int j = j0 + u * blockDim.x;
+            if (j < L) out[j] = v[u];
+        }
+    }
+}
+
+template <bool GEN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
+    sht_anal_pair_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
+                         double *__restrict__ arena, const double2 *__restrict__ tw,
+                         const int *__restrict__ perm, const double2 *__restrict__ W,
+                         const double2 *__restrict__ grid, const double *__restrict__ weights,
+                         int r_begin, int r_count, const int *__restrict__ node_y, int ew,
+                         const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned rank = cl.block_rank();
+    extern __shared__ __align__(16) double2 dsm[];
+    const int L = d.L, Lb = d.Lb;
+    double2 *own = dsm;
+    const int rr = blockIdx.x >> 1;
+    const double2 *src = grid + (int64_t)(rank ? r_count - 1 - rr : r_count + rr) * L;
+    if (d.blue) {
+        for (int i = threadIdx.x; i < Lb; i += blockDim.x) own[i] = make_double2(0.0, 0.0);
+        __syncthreads();
+    }
+    constexpr int kBatch = 4;   // issue a batch of loads before using any
+    for (int j0 = threadIdx.x; j0 < L; j0 += kBatch * blockDim.x) {
+        double2 u[kBatch];
+        int p[kBatch];
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int j = j0 + i * blockDim.x;
+            if (j < L) {
+                p[i] = perm[j];
+                u[i] = src[j];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kBatch; ++i) {
+            const int j = j0 + i * blockDim.x;
+            if (j < L) own[p[i]] = d.blue ? cmul(u[i], chirp[j]) : u[i];
+        }
+    }
+    __syncthreads();
+    row_dft<GEN>(own, 1, d, W, W + Lb, H, false);
+    cl.sync();   // both spectra ready
+    const double2 *peer = cl.map_shared_rank(dsm, rank ^ 1u);
+    const double2 *bU = rank ? peer : own, *bL = rank ? own : peer;
+    const int r = r_begin + rr;
+    const double w = weights[n + r];
+    const double invL = 1.0 / (double)L;
+    const int nord = 2 * n, half = (nord + 1) >> 1;
+    const int a_lo = rank ? half : 0, a_hi = rank ? nord : half;
+    for (int am = a_lo + threadIdx.x; am < a_hi; am += blockDim.x) {
+        int yo, ye, xo = 1, xe = 1;
+        if (node_y) {
+            yo = node_y[2 * am];
+            ye = node_y[2 * am + 1];
+        } else {
+            const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
+            yo = ho.ncols > 0 ? ho.y : -1;
+            ye = he.ncols > 0 ? he.y : -1;
+            xo = ho.x;
+            xe = he.x;
+        }
+        const int bn = L - am;
+        const int pa = d.blue ? perm[am] : am, pb = d.blue ? perm[bn] : bn;
+        double2 sa = bU[pa], sb = bL[pa];
+        if (d.blue) {
+            const double2 c = chirp[am];
+            sa = cmul(sa, c);
+            sb = cmul(sb, c);
+        }
+        const double2 tp = tw[am];
+        const double2 cp = make_double2(tp.x, -tp.y);
+        sa = cmul(make_double2(sa.x * invL, sa.y * invL), cp);
+        sb = cmul(make_double2(sb.x * invL, sb.y * invL), cp);
+        double2 na = make_double2(0.0, 0.0), nb = na;
+        if (am > 0) {
+            const double2 tn = tw[bn];
+            const double2 cn = make_double2(tn.x, -tn.y);
+            na = bU[pb];
+            nb = bL[pb];
+            if (d.blue) {
+                const double2 c = chirp[bn];
+                na = cmul(na, c);
+                nb = cmul(nb, c);
+            }
+            na = cmul(make_double2(na.x * invL, na.y * invL), cn);
+            nb = cmul(make_double2(nb.x * invL, nb.y * invL), cn);
+        }
+        if (yo >= 0) {
+            double2 *e = reinterpret_cast<double2 *>(arena + ((int64_t)yo + (int64_t)rr * xo) * ew);
+            e[0] = make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
+            e[1] = am > 0 ? make_double2(w * (na.x - nb.x), w * (na.y - nb.y))
+                          : make_double2(0.0, 0.0);
+        }
+        if (ye >= 0) {
+            double2 *e = reinterpret_cast<double2 *>(arena + ((int64_t)ye + (int64_t)rr * xe) * ew);
+            e[0] = make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
+            e[1] = am > 0 ? make_double2(w * (na.x + nb.x), w * (na.y + nb.y))
+                          : make_double2(0.0, 0.0);
+        }
+    }
+    cl.sync();   // the peer has finished reading this CTA's row
+}
+
 __device__ __forceinline__ int64_t coeff_offset(int m, int K) {
     // start of order m in ShtCoeffs.pack() (m ascending from -(K-1)), K = 2N
     if (m <= 0) return (int64_t)(K + m - 1) * (K + m) / 2;
@@ -1083,6 +1302,94 @@ static int dft_grid_limit(const bfsht_plan *pl) {
     return pl->dft_scratch ? (int)(pl->dft_scratch_rows / 2) : (1 << 30);
 }
 
+// Shared-memory ceiling of the 2-CTA-cluster row-pair kernels: two CTAs per
+// SM (228 KB per SM, 1 KB reserved per CTA).  BFSHT_DFT_LEGACY=1 selects the
+// one-CTA row-pair kernels for every length (A/B measurements).
+constexpr int kPairSmemMax = 113 * 1024;
+
+static bool pair_path(const bfsht_plan *pl) {
+    static const bool legacy = std::getenv("BFSHT_DFT_LEGACY") != nullptr;
+    return !legacy && pl->dft_Lb * 16 + pl->dft_gen <= kPairSmemMax;
+}
+
+// Forward DFT stage over row pairs r_begin .. r_begin + r_count - 1: node
+// halves through `halves` (or the row-major Yr array when ystride > 0) ->
+// 2 r_count grid rows.
+static int launch_synth(bfsht_plan *pl, const bf_half *halves, const double *arena, int r_begin,
+                        int r_count, double *grid, int64_t yr, int ystride, int ew,
+                        cudaStream_t st) {
+    const int n = pl->n;
+    const DftDesc d = make_desc(pl);
+    const double2 *tw = reinterpret_cast<const double2 *>(pl->dft_tw);
+    const double2 *W = reinterpret_cast<const double2 *>(pl->dft_w);
+    const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
+    const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
+    double2 *g = reinterpret_cast<double2 *>(grid);
+    if (pair_path(pl)) {
+        const int smem = (int)(pl->dft_Lb * 16) + pl->dft_gen;
+        auto kern = pl->dft_gen ? sht_synth_pair_kernel<true> : sht_synth_pair_kernel<false>;
+        int rc = bf_ensure_smem((const void *)kern, smem);
+        if (rc) return rc;
+        kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw,
+                                                     pl->dft_perm, W, g, yr, ystride, ew, chirp, H);
+    } else {
+        const bool sm = pl->dft_scratch == nullptr;
+        const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
+        const int smem = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
+        auto kern = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
+        int rc = bf_ensure_smem((const void *)kern, smem);
+        if (rc) return rc;
+        kern<<<nblk, kDftThreads, smem, st>>>(
+            d, n, halves, arena, r_begin, r_count, tw, pl->dft_perm, W, g, sm,
+            reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), yr,
+            ystride, ew, chirp, H);
+    }
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+// Inverse DFT stage: 2 r_count grid rows -> weighted node halves
+// (node_y: per-half base with consecutive rows, else through `halves`).
+static int launch_anal(bfsht_plan *pl, const bf_half *halves, double *arena, int r_begin,
+                       int r_count, const double *grid, const double *weights, const int *node_y,
+                       int ew, cudaStream_t st) {
+    const int n = pl->n;
+    const DftDesc d = make_desc(pl);
+    const double2 *tw = reinterpret_cast<const double2 *>(pl->dft_tw);
+    const double2 *W = reinterpret_cast<const double2 *>(pl->dft_w);
+    const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
+    const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
+    const double2 *g = reinterpret_cast<const double2 *>(grid);
+    if (pair_path(pl)) {
+        const int smem = (int)(pl->dft_Lb * 16) + pl->dft_gen;
+        auto kern = pl->dft_gen ? sht_anal_pair_kernel<true> : sht_anal_pair_kernel<false>;
+        int rc = bf_ensure_smem((const void *)kern, smem);
+        if (rc) return rc;
+        kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g,
+                                                     weights, r_begin, r_count, node_y, ew, chirp,
+                                                     H);
+    } else {
+        const bool sm = pl->dft_scratch == nullptr;
+        const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
+        const int64_t nh = 2 * (int64_t)pl->norders;
+        const bool ysm = node_y && sm && dft_y_smem(pl->dft_Lb, nh, pl->dft_gen);
+        const int smem = sm ? (ysm ? dft_anal_smem(pl->dft_Lb, nh, pl->dft_gen)
+                                   : dft_pair_smem(pl->dft_Lb, pl->dft_gen))
+                            : pl->dft_gen;
+        auto kern = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
+        int rc = bf_ensure_smem((const void *)kern, smem);
+        if (rc) return rc;
+        kern<<<nblk, kDftThreads, smem, st>>>(
+            d, n, halves, arena, tw, pl->dft_perm, W, g, weights, r_begin, r_count, sm,
+            reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen),
+            ysm ? node_y : nullptr, (int)nh, ew, chirp, H);
+    }
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
 int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStream_t st) {
     const int n = pl->n;
     int rc = bf_dft_prepare(pl, 4LL * n - 1);
@@ -1094,23 +1401,8 @@ int bf_sht_forward(bfsht_plan *pl, const double *coeffs, double *grid, cudaStrea
     pl->launches += 1;
     rc = bf_alt_apply(pl, BFSHT_FORWARD, st);
     if (rc) return rc;
-    const bool sm = pl->dft_scratch == nullptr;
-    const DftDesc d = make_desc(pl);
-    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
-    {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
-        auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
-        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-        if (rc_) return rc_;
-        kern_<<<nblk, kDftThreads, smem_, st>>>(
-        d, n, pl->layout_fwd, pl->arena, 0, n, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), pl->info[10],
-        2 * pl->norders, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-    }
-    BF_CUDA(cudaGetLastError());
-    pl->launches += 1;
-    return 0;
+    return launch_synth(pl, pl->layout_fwd, pl->arena, 0, n, grid, pl->info[10],
+                        2 * pl->norders, BF_NRHS, st);
 }
 
 int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const double *weights,
@@ -1118,24 +1410,8 @@ int bf_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs, const dou
     const int n = pl->n;
     int rc = bf_dft_prepare(pl, 4LL * n - 1);
     if (rc) return rc;
-    const bool sm = pl->dft_scratch == nullptr;
-    const DftDesc d = make_desc(pl);
-    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
-    const int64_t nh = 2 * (int64_t)pl->norders;
-    const bool ysm = sm && dft_y_smem(pl->dft_Lb, nh, pl->dft_gen);
-    {
-        const int smem_ = sm ? (ysm ? dft_anal_smem(pl->dft_Lb, nh, pl->dft_gen) : dft_pair_smem(pl->dft_Lb, pl->dft_gen)) : pl->dft_gen;
-        auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
-        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-        if (rc_) return rc_;
-        kern_<<<nblk, kDftThreads, smem_, st>>>(
-        d, n, pl->layout_inv, pl->arena, reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-        reinterpret_cast<const double2 *>(pl->dft_w), reinterpret_cast<const double2 *>(grid),
-        weights, 0, n, sm, reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen),
-        ysm ? pl->node_y : nullptr, (int)nh, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-    }
-    BF_CUDA(cudaGetLastError());
-    pl->launches += 1;
+    rc = launch_anal(pl, pl->layout_inv, pl->arena, 0, n, grid, weights, pl->node_y, BF_NRHS, st);
+    if (rc) return rc;
     rc = bf_alt_apply(pl, BFSHT_INVERSE, st);
     if (rc) return rc;
     dim3 g1((n + 255) / 256, 2 * n);
@@ -1343,9 +1619,6 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
     if (rc) return rc;
     const int64_t L = pl->dft_L;
     const int64_t ncoef = 4LL * n * n, ngrid = 2LL * n * L;
-    const bool sm = pl->dft_scratch == nullptr;
-    const DftDesc d = make_desc(pl);
-    const int nblk = std::min(std::min(n, pl->sm_count), dft_grid_limit(pl));
     dim3 g1((n + 255) / 256, 2 * n);
     if (dir == BFSHT_FORWARD) {
         for (int b = 0; b < ew / BF_NRHS; ++b) {
@@ -1357,41 +1630,15 @@ int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,
         rc = bf_alt_apply_wide(pl, BFSHT_FORWARD, work, st);
         if (rc) return rc;
         for (int b = 0; b < B; ++b) {
-            {
-                const int smem_ = sm ? dft_pair_smem(L, pl->dft_gen) : pl->dft_gen;
-                auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
-                int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-                if (rc_) return rc_;
-                kern_<<<nblk, kDftThreads, smem_, st>>>(
-                d, n, pl->layout_fwd, work + BF_NRHS * b, 0, n,
-                reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-                reinterpret_cast<const double2 *>(pl->dft_w),
-                reinterpret_cast<double2 *>(out) + b * ngrid, sm,
-                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen), pl->info[10],
-                2 * pl->norders, ew, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-            }
-            BF_CUDA(cudaGetLastError());
-            pl->launches += 1;
+            rc = launch_synth(pl, pl->layout_fwd, work + BF_NRHS * b, 0, n, out + 2 * b * ngrid,
+                              pl->info[10], 2 * pl->norders, ew, st);
+            if (rc) return rc;
         }
     } else {
-        const int64_t nh = 2 * (int64_t)pl->norders;
-        const bool ysm = sm && dft_y_smem(L, nh, pl->dft_gen);
         for (int b = 0; b < B; ++b) {
-            {
-                const int smem_ = sm ? (ysm ? dft_anal_smem(L, nh, pl->dft_gen) : dft_pair_smem(L, pl->dft_gen)) : pl->dft_gen;
-                auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
-                int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-                if (rc_) return rc_;
-                kern_<<<nblk, kDftThreads, smem_, st>>>(
-                d, n, pl->layout_inv, work + BF_NRHS * b,
-                reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-                reinterpret_cast<const double2 *>(pl->dft_w),
-                reinterpret_cast<const double2 *>(in) + b * ngrid, weights, 0, n, sm,
-                reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(L, pl->dft_gen),
-                ysm ? pl->node_y : nullptr, (int)nh, ew, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-            }
-            BF_CUDA(cudaGetLastError());
-            pl->launches += 1;
+            rc = launch_anal(pl, pl->layout_inv, work + BF_NRHS * b, 0, n, in + 2 * b * ngrid,
+                             weights, pl->node_y, ew, st);
+            if (rc) return rc;
         }
         rc = bf_alt_apply_wide(pl, BFSHT_INVERSE, work, st);
         if (rc) return rc;
@@ -1435,22 +1682,7 @@ int bf_synth_rows(bfsht_plan *pl, const bf_half *halves, const double *ybuf, int
     int rc = bf_dft_prepare(pl, 4LL * n - 1);
     if (rc) return rc;
     if (r_count <= 0) return 0;
-    const bool sm = pl->dft_scratch == nullptr;
-    const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
-        auto kern_ = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
-        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-        if (rc_) return rc_;
-        kern_<<<nblk, kDftThreads, smem_, st>>>(
-        make_desc(pl), n, halves, ybuf, r_begin, r_count,
-        reinterpret_cast<const double2 *>(pl->dft_tw), pl->dft_perm,
-        reinterpret_cast<double2 *>(pl->dft_w), reinterpret_cast<double2 *>(grid), sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), (int64_t)0, 0, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-    }
-    BF_CUDA(cudaGetLastError());
-    pl->launches += 1;
-    return 0;
+    return launch_synth(pl, halves, ybuf, r_begin, r_count, grid, 0, 0, BF_NRHS, st);
 }
 
 int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begin, int r_count,
@@ -1459,20 +1691,5 @@ int bf_anal_rows(bfsht_plan *pl, const bf_half *halves, double *ubuf, int r_begi
     int rc = bf_dft_prepare(pl, 4LL * n - 1);
     if (rc) return rc;
     if (r_count <= 0) return 0;
-    const bool sm = pl->dft_scratch == nullptr;
-    const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-    {
-        const int smem_ = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
-        auto kern_ = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
-        int rc_ = bf_ensure_smem((const void *)kern_, smem_);
-        if (rc_) return rc_;
-        kern_<<<nblk, kDftThreads, smem_, st>>>(
-        make_desc(pl), n, halves, ubuf, reinterpret_cast<const double2 *>(pl->dft_tw),
-        pl->dft_perm, reinterpret_cast<const double2 *>(pl->dft_w),
-        reinterpret_cast<const double2 *>(grid), weights, r_begin, r_count, sm,
-        reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), nullptr, 0, BF_NRHS, reinterpret_cast<const double2 *>(pl->dft_chirp), reinterpret_cast<const double2 *>(pl->dft_hhat));
-    }
-    BF_CUDA(cudaGetLastError());
-    pl->launches += 1;
-    return 0;
+    return launch_anal(pl, halves, ubuf, r_begin, r_count, grid, weights, nullptr, BF_NRHS, st);
 }

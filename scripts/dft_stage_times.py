@@ -53,8 +53,6 @@ for n in [int(v) for v in args.n.split(",")]:
     lib, st = run.lib, run._stream()
     run.ybuf.normal_()
     grid = torch.randn((2 * n, L), dtype=torch.complex128, device="cuda")
-    info = (ctypes.c_int64 * 8)()
-    lib.bfsht_dft_info(run.ctx.handle, info)
     # node halves: every present (order, parity) half, n rows x 32 B
     lay = run.layout
     halves = int((lay["ncols"] > 0).sum())
@@ -69,9 +67,8 @@ for n in [int(v) for v in args.n.split(",")]:
         gbs = nbytes / (ms * 1e-3) / 1e9
         print(json.dumps({"n": n, "L": L, "kernel": name, "ms": ms, "alg_bytes": nbytes,
                           "GBps": gbs, "frac_of_peak": gbs / pk,
-                          "row": {"Lb": info[1], "bluestein": bool(info[2]), "R": info[3],
-                                  "S": info[4], "A": info[5], "smem": info[6],
-                                  "threads": info[7]}}), flush=True)
+                          "path": "legacy" if os.environ.get("BFSHT_DFT_LEGACY") else "cluster"}),
+              flush=True)
     run.close()
     del grid, run
     torch.cuda.empty_cache()
