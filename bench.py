@@ -550,7 +550,8 @@ def run_fields(args):
     """BASELINE config C4: batched forward ALT, N=1024, F=64 fields sharing
     one factorization (every order m = 0..2N-1), coefficients complex128
     iid N(0,1).  Step = forward ALT of all fields over all orders
-    (DevicePlan.alt_fields: 8 fields per payload pass on the 16-RHS engine).
+    (DevicePlan.alt_fields: 32 fields per payload pass on the group engine,
+    4 warps sharing each staged tile; 8 per pass with regeneration).
     value = fields/s; roofline = fp64 tensor-core flops (2 flops per stored
     value per real RHS, 2F real RHS) vs cuBLAS DGEMM."""
     import torch
@@ -623,6 +624,8 @@ def run_fields(args):
     cpu_fields_per_s = nf / (t_cpu * w_all / w_sample)
 
     values = dp.stats["payload_values"]
+    fpp = 32 if (nf > 8 and not args.regen
+                 and not os.environ.get("BFSHT_FIELDS_WIDE16")) else 8
     flops = 2.0 * values * 2 * nf
     peak = fp64_gemm_peak(torch, dev)
     achieved = flops / (ms * 1e-3) / 1e12
@@ -635,7 +638,8 @@ def run_fields(args):
                                f"tol {args.tol:g}",
                    "n": n, "fields": nf, "rhs_real": 2 * nf,
                    "payload_values": int(values),
-                   "l2": "inputs larger than L2 (payload streamed once per 8 fields)"},
+                   "fields_per_payload_pass": fpp,
+                   "l2": f"inputs larger than L2 (payload streamed once per {fpp} fields)"},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                      "kernel": "alt_stage_kernel<16> (fp64 DMMA m8n8k4, all stages)",

@@ -154,12 +154,17 @@ int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
  * once before first use. */
 #define BFSHT_WIDE_NRHS 16
 
+/* Doubles per arena entry of bfsht_alt_fields' work buffer: info[5] x
+ * BFSHT_FIELDS_NRHS doubles, zeroed once before first use. */
+#define BFSHT_FIELDS_NRHS 64
+
 /* Batched fields (SURVEY 8(b) "API extension", config 4): alt_forward /
  * alt_inverse on (2N-m, F) / (2N, F) complex128 arrays per plan (alt.py:
  * 264-282 applied column by column; the reference supports 2-D right-hand
  * sides only at idbf_apply, butterfly.py:275-292).  in/out are field-minor
  * (row-major L x F) and laid out plan after plan.  The payload is streamed
- * once per 8 fields. */
+ * once per 32 fields (group engine: 4 warps share each staged tile), or
+ * once per 8 fields when F <= 8 or the plan regenerates tiles. */
 int bfsht_alt_fields(bfsht_plan *pl, int dir, int nfields, const double *in, double *out,
                      const double *weights, double *work, void *stream);
 
@@ -196,6 +201,18 @@ int bfsht_sht_inverse(bfsht_plan *pl, const double *grid, double *coeffs,
  * sign -1 (dir FORWARD, numpy fft) or +1 (INVERSE, L*ifft). */
 int bfsht_dft_rows(int64_t L, int64_t rows, int dir, const double *in,
                    double *out, void *stream);
+
+/* Factor construction: one parity half of the order-m ALT
+ * matrix tabulated on GPU `device` — the entry evaluation of the reference
+ * planner's oracle (pkg/src/bfsht/partition.py:91-169 over
+ * kernels/_recur_cy.pyx:18-67), replacing the host table of
+ * bfsht_legendre_half_table (libbfsht_host) bit for bit.  HOST pointers:
+ * x, mant0, exp0 (n nodes), alpha, beta (offset + 2 (ncols-1) steps), out
+ * (n * ncols doubles, written COLUMN-major: entry (r, j) at j * n + r). */
+int bfsht_half_table_device(int device, int64_t m, int64_t offset, int64_t n, int64_t ncols,
+                            const double *x, const double *alpha, const double *beta,
+                            const double *mant0, const int32_t *exp0, double mag_min,
+                            double *out);
 
 /* Kernel launches issued on this plan since creation or the last reset. */
 int64_t bfsht_plan_launches(bfsht_plan *pl);

@@ -43,6 +43,9 @@ def declare(lib):
     lib.bfsht_sht_inverse.argtypes = [_P, _P, _P, _P, _P]
     lib.bfsht_dft_rows.restype = _I
     lib.bfsht_dft_rows.argtypes = [_I64, _I64, _I, _P, _P, _P]
+    lib.bfsht_half_table_device.restype = _I
+    lib.bfsht_half_table_device.argtypes = [_I, _I64, _I64, _I64, _I64, _P, _P, _P, _P, _P,
+                                            ctypes.c_double, _P]
     lib.bfsht_reset_launches.restype = _I
     lib.bfsht_reset_launches.argtypes = [_P]
     for name in ("bfsht_shard_pack", "bfsht_shard_unpack"):
@@ -86,7 +89,8 @@ EXPORTS = (
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
     "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_alt_fields",
     "bfsht_half_apply", "bfsht_sht_batch", "bfsht_alt_apply_wide",
-    "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_plan_launches",
+    "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_half_table_device",
+    "bfsht_plan_launches",
     "bfsht_reset_launches", "bfsht_shard_pack", "bfsht_shard_unpack",
     "bfsht_gather_entries", "bfsht_scatter_entries", "bfsht_synth_rows",
     "bfsht_anal_rows", "bfsht_comm_unique_id", "bfsht_comm_init", "bfsht_comm_free",

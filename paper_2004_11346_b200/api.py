@@ -32,6 +32,7 @@ from .sht import ShtCoeffs, ShtGridValues
 
 FORWARD, INVERSE = 0, 1
 WIDE_NRHS = 16   # BFSHT_WIDE_NRHS
+FIELDS_NRHS = 64   # BFSHT_FIELDS_NRHS
 
 
 @dataclass
@@ -178,10 +179,20 @@ class DevicePlan:
                                      dtype=torch.float64, device=self.device)
         return self._wide
 
+    def fields_arena(self):
+        """Work arena of alt_fields (BFSHT_FIELDS_NRHS doubles per entry),
+        allocated on first use."""
+        if getattr(self, "_fields", None) is None:
+            torch = _torch()
+            self._fields = torch.zeros((max(self.packed.stats["arena"], 1), FIELDS_NRHS),
+                                       dtype=torch.float64, device=self.device)
+        return self._fields
+
     def alt_fields(self, direction, inp, out=None, stream=None):
         """Batched-fields ALT: inp is a device complex128 (rows, F) tensor,
         rows laid out plan after plan (2N-m coefficient rows forward, 2N
-        node rows inverse); one payload pass per 8 fields."""
+        node rows inverse); one payload pass per 32 fields (8 when F <= 8
+        or the plan regenerates tiles)."""
         torch = _torch()
         inp = inp.contiguous()
         if inp.dim() != 2:
@@ -194,7 +205,7 @@ class DevicePlan:
         check(self.lib, self.lib.bfsht_alt_fields(
             self.handle, direction, nf, ctypes.c_void_p(inp.data_ptr()),
             ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(w),
-            ctypes.c_void_p(self.wide_arena().data_ptr()),
+            ctypes.c_void_p(self.fields_arena().data_ptr()),
             _stream_ptr(torch, stream, self.device)), "bfsht_alt_fields")
         return out
 

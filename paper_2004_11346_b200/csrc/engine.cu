@@ -448,14 +448,15 @@ __device__ __forceinline__ void issue(const StageArgs &a, WarpRing<NR> &ring, in
 
 // B fragment of n-group grp at k block ks: lane holds V[k = 4ks + q][rhs =
 // 8grp + g] (columns past the entry width are the n-padding)
-template <int NR>
+template <int VS>
 __device__ __forceinline__ double bfrag(const double *Vb, int ks, int grp, bool bl) {
-    return bl ? Vb[ks * 4 * NR + grp * 8] : 0.0;
+    return bl ? Vb[ks * 4 * VS + grp * 8] : 0.0;
 }
 
 // Tile product of one op into fragments e: e[grp][mt][0..1] = result row
-// 8mt + lane/4, RHS 8grp + 2(lane%4), +1.
-template <int NR>
+// 8mt + lane/4, RHS 8grp + 2(lane%4), +1.  V: input entries VS doubles
+// apart (the warp's NR-wide slice of a wider entry when VS > NR).
+template <int NR, int VS = NR>
 __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, const double *V,
                                              const double *Z, int lane,
                                              double e[Width<NR>::G][4][2]) {
@@ -467,7 +468,7 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) e[gr][mt][0] = e[gr][mt][1] = 0.0;
     const bool bl = g < Width<NR>::GACT;
-    const double *Vb = V + q * NR + (NR >= 8 ? g : (g & (NR - 1)));
+    const double *Vb = V + q * VS + (NR >= 8 ? g : (g & (NR - 1)));
     if (op.R == BF_T && op.C == BF_T) {
         // full tile: straight-line, all fragment offsets are immediates
         if (op.kind == BF_OP_TILE_N) {
@@ -479,7 +480,7 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
                 for (int mt = 0; mt < 4; ++mt) av[mt] = Ta[(mt * 16 + ks) * 16];
 #pragma unroll
                 for (int gr = 0; gr < G; ++gr) {
-                    const double b = bfrag<NR>(Vb, ks, gr, bl);
+                    const double b = bfrag<VS>(Vb, ks, gr, bl);
 #pragma unroll
                     for (int mt = 0; mt < 4; ++mt) dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);
                 }
@@ -493,7 +494,7 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
                 for (int mt = 0; mt < 4; ++mt) av[mt] = Ta[(ks * 8 + 2 * mt) * 16];
 #pragma unroll
                 for (int gr = 0; gr < G; ++gr) {
-                    const double b = bfrag<NR>(Vb, ks, gr, bl);
+                    const double b = bfrag<VS>(Vb, ks, gr, bl);
 #pragma unroll
                     for (int mt = 0; mt < 4; ++mt) dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);
                 }
@@ -539,7 +540,7 @@ __device__ __forceinline__ void tile_product(const bf_op &op, const double *T, c
             p[mt] += st[mt];                                                   \
         }                                                                      \
         _Pragma("unroll") for (int gr = 0; gr < G; ++gr) {                     \
-            const double b = bfrag<NR>(Vb, ks, gr, bl);                        \
+            const double b = bfrag<VS>(Vb, ks, gr, bl);                        \
             _Pragma("unroll") for (int mt = 0; mt < NMT; ++mt)                 \
                 dmma(e[gr][mt][0], e[gr][mt][1], av[mt], b);                   \
         }                                                                      \
@@ -715,7 +716,301 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
     }
 }
 
+// ------------------------------------------------------------ group engine
+// Batched fields with many fields per payload pass (BASELINE config 4, the
+// "real dense contraction" of north_star (2)).  The warp engine above gives
+// each warp its own op stream, so a staged tile meets only the 16 RHS of
+// one wide entry (8 complex fields) and 64 fields stream the payload 8
+// times at 4 flop/B — below the fp64 ridge.  Here kGW warps form a group
+// that walks ONE op stream through ONE ring: warp w of the group computes
+// RHS [16w, 16w + 16) of every 64-wide arena entry (fields 8w .. 8w+7 of a
+// 32-field pass), so each tile fetched from HBM feeds kGW x 16 RHS and 64
+// fields need 2 payload passes.  Warp 0 of the group is also the producer:
+// it claims tasks, issues the tile and the 512-byte input entries as TMA
+// bulk copies (per-lane bulk copies for gathered inputs) into a free slot,
+// and publishes the op record in the slot; a slot is refilled only after
+// all kGW warps have released it (empty mbarrier, kGW arrivals).  Per-warp
+// accumulation, summation order and stores are those of the warp engine,
+// so results are bitwise those of the 16-wide path.  Plans with
+// regenerated tiles use the 16-wide path (regen is a per-warp step).
+constexpr int kGW = 4;                  // warps per group
+constexpr int kGroups = 2;              // groups per CTA (register-bound)
+constexpr int kGS = 3;                  // ring slots per group
+constexpr int kGNR = kGW * 16;          // doubles per arena entry (BFSHT_FIELDS_NRHS)
+constexpr uint8_t kOpStop = 0xff;       // end-of-stream record
+
+struct alignas(128) GroupRing {
+    double tile[kGS][kTileDoubles];
+    double vec[kGS][BF_T * kGNR];
+    int8_t map[kGS][BF_SLOTS];
+    double zero[16];
+    bf_op meta[kGS];
+    int4 tmeta[kGS];
+    unsigned long long full[kGS], empty[kGS];
+};
+struct alignas(128) GroupScratch {
+    double s[BF_T * 16];                // per-warp placement staging
+};
+constexpr size_t kGroupSmem = sizeof(GroupRing) * kGroups + sizeof(GroupScratch) * kGroups * kGW;
+static_assert(kGroupSmem <= 227 * 1024, "group ring exceeds shared memory");
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Producer side of one op into slot s (whole producer warp).
+__device__ __forceinline__ void group_issue(const StageArgs &a, GroupRing &ring, int s,
+                                            const Rec &r, int gsrc, int lane) {
+    const bf_op &op = r.op;
+    const bool gather = (op.flags & BF_OPF_GATHER) != 0;
+    const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
+    constexpr uint32_t kEntry = kGNR * 8u;
+    int nvec;
+    uint32_t bytes = 0;
+    if (op.kind == BF_OP_ADD) {
+        nvec = op.R;
+    } else {
+        nvec = (op.kind == BF_OP_TILE_N) ? op.C : op.R;
+        bytes += (uint32_t)bf_tile_doubles(op.R, op.C) * 8u;
+    }
+    int nsrc = 0;   // gathered entries present (sources < 0 are skipped)
+    if (gather) {
+        const unsigned has = __ballot_sync(0xffffffffu, lane < nvec && gsrc >= 0);
+        nsrc = __popc(has);
+    }
+    bytes += gather ? (uint32_t)nsrc * kEntry : (uint32_t)nvec * kEntry;
+    if (lanemap) bytes += BF_SLOTS;
+    if (gather && lane < nvec && gsrc < 0) {
+        // absent source (index-add lanes without a skeleton entry): zeros,
+        // written before the arrive that publishes the slot
+        double *d = ring.vec[s] + lane * kGNR;
+        for (int k = 0; k < kGNR; k += 2)
+            *reinterpret_cast<double2 *>(d + k) = make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        ring.meta[s] = op;
+        ring.tmeta[s] = make_int4(r.out, r.nout, r.last, 0);
+        mbar_arrive_tx(&ring.full[s], bytes);
+    }
+    // the slot was last read through the generic proxy; order those reads
+    // before this thread's bulk (async-proxy) writes into it
+    fence_proxy_async();
+    __syncwarp();
+    if (op.kind != BF_OP_ADD && lane == 0)
+        bulk_g2s(ring.tile[s], a.tiles + op.tile, (uint32_t)bf_tile_doubles(op.R, op.C) * 8u,
+                 &ring.full[s]);
+    if (gather) {
+        if (lane < nvec && gsrc >= 0)
+            bulk_g2s(ring.vec[s] + lane * kGNR, a.arena + (int64_t)gsrc * kGNR, kEntry,
+                     &ring.full[s]);
+    } else if (lane == 1 && nvec > 0) {
+        bulk_g2s(ring.vec[s], a.arena + (int64_t)op.in * kGNR, (uint32_t)nvec * kEntry,
+                 &ring.full[s]);
+    }
+    if (lanemap && lane == 2)
+        bulk_g2s(ring.map[s], a.maps + (int64_t)op.aux * BF_SLOTS, BF_SLOTS, &ring.full[s]);
+}
+
+__global__ void __launch_bounds__(kGroups * kGW * 32, 1) alt_group_kernel(StageArgs a) {
+    constexpr int NR = 16, G = 2, QACT = 4;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gid = warp / kGW, wg = warp % kGW;
+    GroupRing &ring = reinterpret_cast<GroupRing *>(smem_raw)[gid];
+    double *S = reinterpret_cast<GroupScratch *>(smem_raw + sizeof(GroupRing) * kGroups)[warp].s;
+    {
+        // zero the rings once (padded tile columns multiply stale entries,
+        // which must be finite) and init the barriers
+        double2 *z = reinterpret_cast<double2 *>(smem_raw);
+        for (int i = threadIdx.x; i < (int)(kGroupSmem / sizeof(double2)); i += blockDim.x)
+            z[i] = make_double2(0.0, 0.0);
+        __syncthreads();
+        if (wg == 0 && lane == 0) {
+            for (int s = 0; s < kGS; ++s) {
+                mbar_init(&ring.full[s], 1);
+                mbar_init(&ring.empty[s], kGW);
+            }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    const int g = lane >> 2, q = lane & 3;
+    const bool producer = wg == 0;
+
+    Cursor cur;
+    Rec q0, q1;
+    int g0 = -1;
+    uint32_t seq_issue = 0, seq_use = 0;
+    bool stopped = false;
+    if (producer) {
+        cur.n = cur.i = 0;
+        cur.base = cur.out = cur.nout = 0;
+        cur.nt = bcast(claim_raw(a, lane));
+        cur.raw = 0;
+        if (cur.nt < a.ntasks) {
+            cur.ntask = load_task(a, cur.nt);
+            cur.raw = claim_raw(a, lane);
+        }
+        q0 = advance(a, cur, lane);
+        g0 = gather_src(a, q0, lane);
+        q1 = advance(a, cur, lane);
+    }
+    // producer: fill free slots; the stream ends with one stop record
+    auto produce = [&]() {
+        while (!stopped && seq_issue - seq_use < kGS) {
+            const int s = seq_issue % kGS;
+            if (seq_issue >= kGS) mbar_wait(&ring.empty[s], ((seq_issue / kGS) - 1) & 1u);
+            if (q0.valid) {
+                group_issue(a, ring, s, q0, g0, lane);
+                q0 = q1;
+                g0 = gather_src(a, q0, lane);
+                q1 = advance(a, cur, lane);
+            } else {
+                if (lane == 0) {
+                    ring.meta[s].kind = kOpStop;
+                    mbar_arrive_tx(&ring.full[s], 0);
+                }
+                stopped = true;
+            }
+            ++seq_issue;
+            __syncwarp();
+        }
+    };
+    if (producer) produce();
+
+    double acc[G][8][2];
+#pragma unroll
+    for (int gr = 0; gr < G; ++gr)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[gr][j][0] = acc[gr][j][1] = 0.0;
+
+    for (;;) {
+        const int s = seq_use % kGS;
+        mbar_wait(&ring.full[s], (seq_use / kGS) & 1u);
+        ++seq_use;
+        const bf_op op = ring.meta[s];
+        if (op.kind == kOpStop) break;
+        const int4 tm = ring.tmeta[s];
+        const double *V = ring.vec[s] + wg * 16;
+        if (op.kind == BF_OP_ADD) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int jj = 8 * j + g - op.off;
+                if (q < QACT && jj >= 0 && jj < op.R) {
+#pragma unroll
+                    for (int gr = 0; gr < G; ++gr) {
+                        const double2 v =
+                            *reinterpret_cast<const double2 *>(V + jj * kGNR + gr * 8 + 2 * q);
+                        acc[gr][j][0] += v.x;
+                        acc[gr][j][1] += v.y;
+                    }
+                }
+            }
+        } else {
+            double e[G][4][2];
+            tile_product<NR, kGNR>(op, ring.tile[s], V, ring.zero, lane, e);
+            const bool lanemap = (op.flags & BF_OPF_LANEMAP) != 0;
+            if (!lanemap && (op.off & 7) == 0) {
+                switch (op.off >> 3) {
+                    case 0: place_tiles<G, 0>(acc, e); break;
+                    case 1: place_tiles<G, 1>(acc, e); break;
+                    case 2: place_tiles<G, 2>(acc, e); break;
+                    case 3: place_tiles<G, 3>(acc, e); break;
+                    case 4: place_tiles<G, 4>(acc, e); break;
+                    case 5: place_tiles<G, 5>(acc, e); break;
+                    case 6: place_tiles<G, 6>(acc, e); break;
+                    default: place_tiles<G, 7>(acc, e); break;
+                }
+            } else {
+                const int width = (op.kind == BF_OP_TILE_N) ? op.R : op.C;
+                const int MT = (width + 7) >> 3;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+                    if (mt < MT && q < QACT) {
+#pragma unroll
+                        for (int gr = 0; gr < G; ++gr)
+                            *reinterpret_cast<double2 *>(S + (8 * mt + g) * NR + gr * 8 + 2 * q) =
+                                make_double2(e[gr][mt][0], e[gr][mt][1]);
+                    }
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int sl = 8 * j + g;
+                    const int src = lanemap ? (int)ring.map[s][sl] : sl - op.off;
+                    if (q < QACT && src >= 0 && src < width) {
+#pragma unroll
+                        for (int gr = 0; gr < G; ++gr) {
+                            const double2 v =
+                                *reinterpret_cast<const double2 *>(S + src * NR + gr * 8 + 2 * q);
+                            acc[gr][j][0] += v.x;
+                            acc[gr][j][1] += v.y;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (tm.z) {
+            const int nout = tm.y & 0xff;
+            const int stride = (tm.y >> 8) ? (tm.y >> 8) : 1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int sl = 8 * j + g;
+                if (q < QACT && sl < nout) {
+                    double *o = a.arena + ((int64_t)tm.x + (int64_t)sl * stride) * kGNR + wg * 16 +
+                                2 * q;
+#pragma unroll
+                    for (int gr = 0; gr < G; ++gr)
+                        *reinterpret_cast<double2 *>(o + gr * 8) =
+                            make_double2(acc[gr][j][0], acc[gr][j][1]);
+                }
+#pragma unroll
+                for (int gr = 0; gr < G; ++gr) acc[gr][j][0] = acc[gr][j][1] = 0.0;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.empty[s]);
+        if (producer) produce();
+    }
+}
+
 }  // namespace
+
+// All stages of one direction over a 64-wide arena (group engine).
+int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) {
+    const std::vector<int64_t> &b = pl->stages[dir];
+    const int nst = (int)b.size() - 1;
+    if (pl->ncounters < nst) {
+        bfsht_set_error("plan counters not allocated");
+        return -3;
+    }
+    int rc = bf_ensure_smem((const void *)alt_group_kernel, (int)kGroupSmem);
+    if (rc) return rc;
+    for (int s = 0; s < nst; ++s) {
+        if (b[s + 1] <= b[s]) continue;
+        StageArgs a;
+        a.tiles = pl->tiles;
+        a.ops = pl->ops;
+        a.idx = pl->idx;
+        a.maps = pl->maps;
+        a.tasks = pl->tasks;
+        a.arena = arena;
+        a.t0 = b[s];
+        a.ntasks = b[s + 1] - b[s];
+        a.counter = pl->counters + s;
+        a.rec = pl->rec;
+        a.xpos = pl->xpos;
+        std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
+        BF_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), st));
+        const int64_t want = (a.ntasks + kGroups - 1) / kGroups;
+        const int grid = (int)(want < pl->sm_count ? want : pl->sm_count);
+        alt_group_kernel<<<grid, kGroups * kGW * 32, kGroupSmem, st>>>(a);
+        BF_CUDA(cudaGetLastError());
+        pl->launches += 1;
+    }
+    return 0;
+}
 
 template <int NR>
 static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, double *arena,

@@ -94,6 +94,7 @@ int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter,
                  cudaStream_t s, int max_ctas);
 int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
 int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);
+int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);
 int bf_alt_fields(bfsht_plan *pl, int dir, int F, const double *in, double *out,
                   const double *weights, double *work, cudaStream_t st);
 int bf_sht_batch(bfsht_plan *pl, int dir, int B, const double *in, double *out,

@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <algorithm>
 #include <complex>
 #include <vector>
@@ -37,6 +38,9 @@ constexpr int kMaxRadix = 24;
 #define BF_DFT_THREADS 256
 #endif
 constexpr int kDftThreads = BF_DFT_THREADS;
+// shared-memory ceiling of a one-row CTA: two CTAs per SM (228 KB per SM,
+// 1 KB reserved per CTA)
+constexpr int kPairSmemMax = 113 * 1024;
 
 struct DftDesc {
     int L;       // transform length
@@ -838,20 +842,134 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
     }
 }
 
-template <bool GEN>
+// Forward, one row per CTA without a cluster: each CTA reads the node
+// halves of every order for its row (the pair's second read of the same
+// entries is an L2 hit, both CTAs run together) and assembles g_e + g_o
+// (row n+r) or g_e - g_o (row n-1-r).  SM: the row in shared memory
+// (grid = 2 * r_count); else in a global (L2-resident) scratch row per
+// CTA, persistent over the rows — the path of rows too long for shared
+// memory (N >= 2048), at 128 registers so two CTAs share an SM.
+template <bool SM, bool GEN>
+__global__ void __launch_bounds__(kDftThreads, 2)
+    sht_synth_row_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
+                         const double *__restrict__ arena, int r_count,
+                         const double2 *__restrict__ tw, const int *__restrict__ perm,
+                         const double2 *__restrict__ W, double2 *__restrict__ grid, int64_t yr,
+                         int ystride, int ew, const double2 *__restrict__ chirp,
+                         const double2 *__restrict__ H, double2 *scratch) {
+    const int L = d.L, Lb = d.Lb;
+    double2 *buf = dft_buffer<SM>(scratch, 1, Lb);
+    const int nord = 2 * n;
+    for (int t = blockIdx.x; t < 2 * r_count; t += gridDim.x) {
+        const int rr = t >> 1;
+        const bool lower = t & 1;
+        if (d.blue) {
+            for (int i = threadIdx.x; i < Lb; i += blockDim.x) buf[i] = make_double2(0.0, 0.0);
+            __syncthreads();
+        }
+        constexpr int kBatch = 2;
+        for (int a0 = threadIdx.x; a0 < nord; a0 += kBatch * blockDim.x) {
+            double2 op[kBatch], on[kBatch], ep[kBatch], en[kBatch], tp[kBatch], tn[kBatch];
+            int pp[kBatch], pn[kBatch];
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) {
+                const int am = a0 + i * blockDim.x;
+                const bool ok = am < nord;
+                op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
+                if (ok) {
+                    const double2 *eo = nullptr, *ee = nullptr;
+                    if (ystride > 0) {
+                        const double *rowp = arena + (yr + (int64_t)rr * ystride) * ew;
+                        eo = reinterpret_cast<const double2 *>(rowp + (2 * am) * ew);
+                        ee = reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew);
+                    } else {
+                        const bf_half ho = halves[2 * am], he = halves[2 * am + 1];
+                        if (ho.ncols > 0)
+                            eo = reinterpret_cast<const double2 *>(
+                                arena + ((int64_t)ho.y + (int64_t)rr * ho.x) * ew);
+                        if (he.ncols > 0)
+                            ee = reinterpret_cast<const double2 *>(
+                                arena + ((int64_t)he.y + (int64_t)rr * he.x) * ew);
+                    }
+                    if (eo) {
+                        op[i] = eo[0];
+                        on[i] = eo[1];
+                    }
+                    if (ee) {
+                        ep[i] = ee[0];
+                        en[i] = ee[1];
+                    }
+                }
+                const int bn = am > 0 && ok ? L - am : 0;
+                tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
+                tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
+                if (d.blue && ok) {
+                    tp[i] = cmul(tp[i], conjif(chirp[am], true));
+                    tn[i] = cmul(tn[i], conjif(chirp[bn], true));
+                }
+                pp[i] = ok ? perm[am] : 0;
+                pn[i] = ok ? perm[bn] : 0;
+            }
+#pragma unroll
+            for (int i = 0; i < kBatch; ++i) {
+                const int am = a0 + i * blockDim.x;
+                if (am < nord) {
+                    const double2 vp = lower ? make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y)
+                                             : make_double2(ep[i].x + op[i].x, ep[i].y + op[i].y);
+                    buf[pp[i]] = cmul(vp, tp[i]);
+                    if (am > 0) {
+                        const double2 vn = lower
+                                               ? make_double2(en[i].x - on[i].x, en[i].y - on[i].y)
+                                               : make_double2(en[i].x + on[i].x, en[i].y + on[i].y);
+                        buf[pn[i]] = cmul(vn, tn[i]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        row_dft<GEN>(buf, 1, d, W, W + Lb, H, true);
+        double2 *out = grid + (int64_t)(lower ? r_count - 1 - rr : r_count + rr) * L;
+        for (int j0 = threadIdx.x; j0 < L; j0 += 2 * blockDim.x) {
+            double2 v[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int j = j0 + u * blockDim.x;
+                if (j < L) {
+                    v[u] = buf[d.blue ? perm[j] : j];
+                    if (d.blue) v[u] = cmul(v[u], conjif(chirp[j], true));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int j = j0 + u * blockDim.x;
+                if (j < L) out[j] = v[u];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// SM = false: each CTA's row lives in a global (L2-resident) scratch row,
+// the cluster persistent over row pairs; the peer's row is read through
+// global memory after the cluster barrier (release / acquire at cluster
+// scope orders those accesses).
+template <bool SM, bool GEN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
     sht_anal_pair_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
                          double *__restrict__ arena, const double2 *__restrict__ tw,
                          const int *__restrict__ perm, const double2 *__restrict__ W,
                          const double2 *__restrict__ grid, const double *__restrict__ weights,
                          int r_begin, int r_count, const int *__restrict__ node_y, int ew,
-                         const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
+                         const double2 *__restrict__ chirp, const double2 *__restrict__ H,
+                         double2 *scratch) {
     cg::cluster_group cl = cg::this_cluster();
     const unsigned rank = cl.block_rank();
     extern __shared__ __align__(16) double2 dsm[];
     const int L = d.L, Lb = d.Lb;
-    double2 *own = dsm;
-    const int rr = blockIdx.x >> 1;
+    double2 *own = SM ? dsm : scratch + (int64_t)blockIdx.x * Lb;
+    const double2 *peer = SM ? cl.map_shared_rank(dsm, rank ^ 1u)
+                             : scratch + (int64_t)(blockIdx.x ^ 1u) * Lb;
+    for (int rr = blockIdx.x >> 1; rr < r_count; rr += gridDim.x >> 1) {
     const double2 *src = grid + (int64_t)(rank ? r_count - 1 - rr : r_count + rr) * L;
     if (d.blue) {
         for (int i = threadIdx.x; i < Lb; i += blockDim.x) own[i] = make_double2(0.0, 0.0);
@@ -878,7 +996,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
     __syncthreads();
     row_dft<GEN>(own, 1, d, W, W + Lb, H, false);
     cl.sync();   // both spectra ready
-    const double2 *peer = cl.map_shared_rank(dsm, rank ^ 1u);
     const double2 *bU = rank ? peer : own, *bL = rank ? own : peer;
     const int r = r_begin + rr;
     const double w = weights[n + r];
@@ -937,6 +1054,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
         }
     }
     cl.sync();   // the peer has finished reading this CTA's row
+    }
 }
 
 __device__ __forceinline__ int64_t coeff_offset(int m, int K) {
@@ -1286,10 +1404,9 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     pl->dft_blue = blue;
     pl->dft_gen = dft_gen_bytes(rad);
     const int gen = pl->dft_gen;
-    const int need = dft_smem_bytes(Lb, 2);
-    int maxsm = 0;
-    BF_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, pl->device));
-    if (need + gen > maxsm) {
+    // global scratch rows for rows longer than half an SM's shared memory
+    // (the legacy one-CTA pair kernels use it when two rows exceed a CTA's)
+    if (Lb * 16 + gen > kPairSmemMax) {
         const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
         BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * Lb * rows));
         pl->dft_scratch_rows = rows;
@@ -1302,14 +1419,26 @@ static int dft_grid_limit(const bfsht_plan *pl) {
     return pl->dft_scratch ? (int)(pl->dft_scratch_rows / 2) : (1 << 30);
 }
 
-// Shared-memory ceiling of the 2-CTA-cluster row-pair kernels: two CTAs per
-// SM (228 KB per SM, 1 KB reserved per CTA).  BFSHT_DFT_LEGACY=1 selects the
-// one-CTA row-pair kernels for every length (A/B measurements).
-constexpr int kPairSmemMax = 113 * 1024;
-
+// DFT-stage kernel choice.  A row in half an SM's shared memory: rows in
+// shared memory, two CTAs per SM (synthesis one row per CTA, analysis a
+// 2-CTA cluster per row pair).  Longer rows: the same kernels over global
+// (L2-resident) scratch rows, persistent.  BFSHT_DFT_LEGACY=1 selects the
+// one-CTA row-pair kernels (both rows in one CTA) for A/B measurements;
+// BFSHT_DFT_SYNTH=cluster the 2-CTA-cluster synthesis for short rows.
+static bool legacy_path() {
+    static const bool v = std::getenv("BFSHT_DFT_LEGACY") != nullptr;
+    return v;
+}
 static bool pair_path(const bfsht_plan *pl) {
-    static const bool legacy = std::getenv("BFSHT_DFT_LEGACY") != nullptr;
-    return !legacy && pl->dft_Lb * 16 + pl->dft_gen <= kPairSmemMax;
+    return !legacy_path() && pl->dft_Lb * 16 + pl->dft_gen <= kPairSmemMax;
+}
+static bool cluster_synth() {
+    static const char *v = std::getenv("BFSHT_DFT_SYNTH");
+    return v && std::strcmp(v, "cluster") == 0;
+}
+static int scratch_grid(const bfsht_plan *pl, int r_count) {
+    const int64_t g = std::min<int64_t>(2LL * r_count, pl->dft_scratch_rows) & ~1LL;
+    return (int)g;
 }
 
 // Forward DFT stage over row pairs r_begin .. r_begin + r_count - 1: node
@@ -1325,15 +1454,28 @@ static int launch_synth(bfsht_plan *pl, const bf_half *halves, const double *are
     const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
     const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
     double2 *g = reinterpret_cast<double2 *>(grid);
-    if (pair_path(pl)) {
+    if (pair_path(pl) && cluster_synth()) {
         const int smem = (int)(pl->dft_Lb * 16) + pl->dft_gen;
         auto kern = pl->dft_gen ? sht_synth_pair_kernel<true> : sht_synth_pair_kernel<false>;
         int rc = bf_ensure_smem((const void *)kern, smem);
         if (rc) return rc;
         kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw,
                                                      pl->dft_perm, W, g, yr, ystride, ew, chirp, H);
+    } else if (!legacy_path()) {
+        const bool sm = pair_path(pl);
+        const int smem = sm ? (int)(pl->dft_Lb * 16) + pl->dft_gen : pl->dft_gen;
+        auto kern = sm ? (pl->dft_gen ? sht_synth_row_kernel<true, true>
+                                      : sht_synth_row_kernel<true, false>)
+                       : (pl->dft_gen ? sht_synth_row_kernel<false, true>
+                                      : sht_synth_row_kernel<false, false>);
+        const int grid = sm ? 2 * r_count : scratch_grid(pl, r_count);
+        int rc = bf_ensure_smem((const void *)kern, smem);
+        if (rc) return rc;
+        kern<<<grid, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw, pl->dft_perm, W, g,
+                                              yr, ystride, ew, chirp, H,
+                                              reinterpret_cast<double2 *>(pl->dft_scratch));
     } else {
-        const bool sm = pl->dft_scratch == nullptr;
+        const bool sm = dft_pair_smem(pl->dft_Lb, pl->dft_gen) <= 227 * 1024;
         const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
         const int smem = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
         auto kern = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
@@ -1361,16 +1503,21 @@ static int launch_anal(bfsht_plan *pl, const bf_half *halves, double *arena, int
     const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
     const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
     const double2 *g = reinterpret_cast<const double2 *>(grid);
-    if (pair_path(pl)) {
-        const int smem = (int)(pl->dft_Lb * 16) + pl->dft_gen;
-        auto kern = pl->dft_gen ? sht_anal_pair_kernel<true> : sht_anal_pair_kernel<false>;
+    if (!legacy_path()) {
+        const bool sm = pair_path(pl);
+        const int smem = sm ? (int)(pl->dft_Lb * 16) + pl->dft_gen : pl->dft_gen;
+        auto kern = sm ? (pl->dft_gen ? sht_anal_pair_kernel<true, true>
+                                      : sht_anal_pair_kernel<true, false>)
+                       : (pl->dft_gen ? sht_anal_pair_kernel<false, true>
+                                      : sht_anal_pair_kernel<false, false>);
+        const int grid = sm ? 2 * r_count : scratch_grid(pl, r_count);
         int rc = bf_ensure_smem((const void *)kern, smem);
         if (rc) return rc;
-        kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g,
-                                                     weights, r_begin, r_count, node_y, ew, chirp,
-                                                     H);
+        kern<<<grid, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g, weights,
+                                              r_begin, r_count, node_y, ew, chirp, H,
+                                              reinterpret_cast<double2 *>(pl->dft_scratch));
     } else {
-        const bool sm = pl->dft_scratch == nullptr;
+        const bool sm = dft_pair_smem(pl->dft_Lb, pl->dft_gen) <= 227 * 1024;
         const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
         const int64_t nh = 2 * (int64_t)pl->norders;
         const bool ysm = node_y && sm && dft_y_smem(pl->dft_Lb, nh, pl->dft_gen);
@@ -1464,7 +1611,7 @@ constexpr int kFPerPass = kW / 2;
 
 __global__ void fields_pack_kernel(int F, int f0, const bf_half *__restrict__ halves,
                                    const int64_t *__restrict__ off, const double2 *__restrict__ in,
-                                   double *__restrict__ arena) {
+                                   double *__restrict__ arena, int ew) {
     const int o = blockIdx.y, f = threadIdx.x;
     const int j = blockIdx.x * blockDim.y + threadIdx.y;
     for (int par = 0; par < 2; ++par) {
@@ -1472,21 +1619,22 @@ __global__ void fields_pack_kernel(int F, int f0, const bf_half *__restrict__ ha
         if (j >= h.ncols) continue;
         double2 v = make_double2(0.0, 0.0);
         if (f0 + f < F) v = in[(off[o] + (par == 0 ? 1 : 0) + 2 * (int64_t)j) * F + f0 + f];
-        *reinterpret_cast<double2 *>(arena + ((int64_t)h.x + j) * kW + 2 * f) = v;
+        *reinterpret_cast<double2 *>(arena + ((int64_t)h.x + j) * ew + 2 * f) = v;
     }
 }
 
 __global__ void fields_assemble_kernel(int n, int F, int f0, const bf_half *__restrict__ layout,
-                                       const double *__restrict__ arena, double2 *__restrict__ out) {
+                                       const double *__restrict__ arena, double2 *__restrict__ out,
+                                       int ew) {
     const int o = blockIdx.y, f = threadIdx.x;
     const int r = blockIdx.x * blockDim.y + threadIdx.y;
     if (r >= n || f0 + f >= F) return;
     const bf_half ho = layout[2 * o], he = layout[2 * o + 1];
     double2 go = make_double2(0.0, 0.0), ge = go;
     if (ho.ncols > 0)
-        go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)r * ho.x) * kW + 2 * f);
+        go = *reinterpret_cast<const double2 *>(arena + ((int64_t)ho.y + (int64_t)r * ho.x) * ew + 2 * f);
     if (he.ncols > 0)
-        ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)r * he.x) * kW + 2 * f);
+        ge = *reinterpret_cast<const double2 *>(arena + ((int64_t)he.y + (int64_t)r * he.x) * ew + 2 * f);
     double2 *col = out + (int64_t)o * 2 * n * F + f0 + f;
     col[(int64_t)(n + r) * F] = make_double2(ge.x + go.x, ge.y + go.y);
     col[(int64_t)(n - 1 - r) * F] = make_double2(ge.x - go.x, ge.y - go.y);
@@ -1494,7 +1642,7 @@ __global__ void fields_assemble_kernel(int n, int F, int f0, const bf_half *__re
 
 __global__ void fields_fold_kernel(int n, int F, int f0, const bf_half *__restrict__ halves,
                                    const double2 *__restrict__ in, const double *__restrict__ weights,
-                                   double *__restrict__ arena) {
+                                   double *__restrict__ arena, int ew) {
     const int o = blockIdx.y, f = threadIdx.x;
     const int r = blockIdx.x * blockDim.y + threadIdx.y;
     if (r >= n) return;
@@ -1507,16 +1655,17 @@ __global__ void fields_fold_kernel(int n, int F, int f0, const bf_half *__restri
     const double w = weights[n + r];
     const bf_half ho = halves[2 * o], he = halves[2 * o + 1];
     if (ho.ncols > 0)
-        *reinterpret_cast<double2 *>(arena + ((int64_t)ho.y + r) * kW + 2 * f) =
+        *reinterpret_cast<double2 *>(arena + ((int64_t)ho.y + r) * ew + 2 * f) =
             make_double2(w * (up.x - lo.x), w * (up.y - lo.y));
     if (he.ncols > 0)
-        *reinterpret_cast<double2 *>(arena + ((int64_t)he.y + r) * kW + 2 * f) =
+        *reinterpret_cast<double2 *>(arena + ((int64_t)he.y + r) * ew + 2 * f) =
             make_double2(w * (up.x + lo.x), w * (up.y + lo.y));
 }
 
 __global__ void fields_unpack_kernel(int F, int f0, const bf_half *__restrict__ halves,
                                      const int64_t *__restrict__ off,
-                                     const double *__restrict__ arena, double2 *__restrict__ out) {
+                                     const double *__restrict__ arena, double2 *__restrict__ out,
+                                     int ew) {
     const int o = blockIdx.y, f = threadIdx.x;
     const int j = blockIdx.x * blockDim.y + threadIdx.y;
     if (f0 + f >= F) return;
@@ -1524,7 +1673,7 @@ __global__ void fields_unpack_kernel(int F, int f0, const bf_half *__restrict__ 
         const bf_half h = halves[2 * o + par];
         if (j >= h.ncols) continue;
         out[(off[o] + (par == 0 ? 1 : 0) + 2 * (int64_t)j) * F + f0 + f] =
-            *reinterpret_cast<const double2 *>(arena + ((int64_t)h.x + j) * kW + 2 * f);
+            *reinterpret_cast<const double2 *>(arena + ((int64_t)h.x + j) * ew + 2 * f);
     }
 }
 
@@ -1547,31 +1696,43 @@ __global__ void half_store_kernel(int64_t base, int64_t stride, int len, int k, 
 
 }  // namespace
 
+// More than 8 fields on a plan without regenerated tiles: passes of 32
+// fields through the group engine (64-wide entries, bf_alt_apply_group);
+// otherwise passes of 8 fields through the 16-wide warp engine.  Both give
+// the same bits (per-field sums in the same order).  BFSHT_FIELDS_WIDE16=1
+// forces the 8-field passes (A/B measurements).
 int bf_alt_fields(bfsht_plan *pl, int dir, int F, const double *in, double *out,
                   const double *weights, double *work, cudaStream_t st) {
     const int n = pl->n, no = pl->norders;
     if (no == 0 || F == 0) return 0;
-    const dim3 blk(kFPerPass, 32);
-    const dim3 g((n + 31) / 32, no);
-    for (int f0 = 0; f0 < F; f0 += kFPerPass) {
+    static const bool force16 = std::getenv("BFSHT_FIELDS_WIDE16") != nullptr;
+    const bool group = F > kFPerPass && pl->info[18] == 0 && !force16;
+    const int ew = group ? BFSHT_FIELDS_NRHS : kW;
+    const int fpp = ew / 2;
+    const dim3 blk(fpp, 256 / fpp);
+    const dim3 g((n + blk.y - 1) / blk.y, no);
+    for (int f0 = 0; f0 < F; f0 += fpp) {
+        auto apply = [&]() {
+            return group ? bf_alt_apply_group(pl, dir, work, st) : bf_alt_apply_wide(pl, dir, work, st);
+        };
         if (dir == BFSHT_FORWARD) {
             fields_pack_kernel<<<g, blk, 0, st>>>(F, f0, pl->halves, pl->order_off,
-                                                  reinterpret_cast<const double2 *>(in), work);
+                                                  reinterpret_cast<const double2 *>(in), work, ew);
             BF_CUDA(cudaGetLastError());
-            int rc = bf_alt_apply_wide(pl, dir, work, st);
+            int rc = apply();
             if (rc) return rc;
             fields_assemble_kernel<<<g, blk, 0, st>>>(n, F, f0, pl->layout_fwd, work,
-                                                      reinterpret_cast<double2 *>(out));
+                                                      reinterpret_cast<double2 *>(out), ew);
             BF_CUDA(cudaGetLastError());
         } else {
             fields_fold_kernel<<<g, blk, 0, st>>>(n, F, f0, pl->halves,
                                                   reinterpret_cast<const double2 *>(in), weights,
-                                                  work);
+                                                  work, ew);
             BF_CUDA(cudaGetLastError());
-            int rc = bf_alt_apply_wide(pl, dir, work, st);
+            int rc = apply();
             if (rc) return rc;
             fields_unpack_kernel<<<g, blk, 0, st>>>(F, f0, pl->halves, pl->order_off, work,
-                                                    reinterpret_cast<double2 *>(out));
+                                                    reinterpret_cast<double2 *>(out), ew);
             BF_CUDA(cudaGetLastError());
         }
         pl->launches += 2;
@@ -1656,7 +1817,7 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
                 cudaStream_t st) {
     int rc = bf_dft_prepare(pl, L);
     if (rc) return rc;
-    const bool sm = dft_smem_bytes(pl->dft_Lb, 1) + pl->dft_gen <= 227 * 1024 && pl->dft_scratch == nullptr;
+    const bool sm = dft_smem_bytes(pl->dft_Lb, 1) + pl->dft_gen <= 227 * 1024;
     int grid = (int)(rows < 4096 ? rows : 4096);
     if (!sm) grid = (int)std::min<int64_t>(grid, pl->dft_scratch_rows);
     if (grid <= 0) return 0;

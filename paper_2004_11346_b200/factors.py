@@ -16,6 +16,7 @@ bitwise identical.  None of this runs on the GPU: the device consumes the
 finished factors through pack.py.
 """
 from dataclasses import dataclass, field
+from functools import lru_cache
 
 import numpy as np
 import scipy.linalg
@@ -215,6 +216,19 @@ def sample_indices(count, total, mode="mock_chebyshev", rng=None):
                                   replace=False)).astype(np.intp)
     if mode != "mock_chebyshev":
         raise ValueError(f"unknown sampling mode {mode!r}")
+    return _mock_chebyshev(count, total)
+
+
+@lru_cache(maxsize=8192)
+def _mock_chebyshev(count, total):
+    # deterministic in (count, total): the planner asks for the same few
+    # shapes thousands of times, so the result is built once (read-only)
+    out = _mock_chebyshev_build(count, total)
+    out.setflags(write=False)
+    return out
+
+
+def _mock_chebyshev_build(count, total):
     t = np.cos(np.pi * (2.0 * np.arange(count, dtype=np.float64) + 1.0)
                / (2.0 * count))
     raw = np.rint((t + 1.0) * 0.5 * (total - 1)).astype(np.intp)

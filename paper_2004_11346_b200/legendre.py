@@ -100,9 +100,16 @@ def _ptr(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def half_table(m, offset, x, ncols):
-    """Dense parity half: out[r, j] = Pbar_{m+offset+2j}^m(x[r])."""
+def half_table(m, offset, x, ncols, device=None):
+    """Dense parity half: out[r, j] = Pbar_{m+offset+2j}^m(x[r]).
+
+    ``device`` (a CUDA ordinal) evaluates the entries on that GPU
+    (bfsht_half_table_device): the same bits, returned as the
+    transpose of a column-major buffer (the planner reads the table only
+    through copies, so its layout does not reach the factors)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
+    if device is not None and x.size and ncols:
+        return _half_table_device(m, offset, x, ncols, int(device))
     out = np.empty((x.size, ncols))
     if x.size == 0 or ncols == 0:
         return out
@@ -117,6 +124,35 @@ def half_table(m, offset, x, ncols):
         m, offset, x.size, ncols, _ptr(x), _ptr(alpha), _ptr(beta),
         _ptr(mant), _ptr(e2), MAG_MIN, _ptr(out))
     return out
+
+
+_DEVICE_USED = False
+
+
+def device_tables_used():
+    """True once this process has tabulated on a GPU (it then holds a CUDA
+    context, so planner workers must not be forked from it)."""
+    return _DEVICE_USED
+
+
+def _half_table_device(m, offset, x, ncols, device):
+    global _DEVICE_USED
+    _DEVICE_USED = True
+    k_last = m + offset + 2 * (ncols - 1)
+    alpha, beta = recurrence_coefficients(m, k_last)
+    alpha = np.ascontiguousarray(alpha)
+    beta = np.ascontiguousarray(beta)
+    mant, e2 = start_values(m, x)
+    mant = np.ascontiguousarray(mant)
+    e2 = np.ascontiguousarray(e2, dtype=np.int32)
+    out = np.empty((ncols, x.size))
+    lib = native.cuda()
+    rc = lib.bfsht_half_table_device(device, m, offset, x.size, ncols, _ptr(x), _ptr(alpha),
+                                     _ptr(beta), _ptr(mant), _ptr(e2), MAG_MIN, _ptr(out))
+    if rc != 0:
+        raise RuntimeError("bfsht_half_table_device: "
+                           + lib.bfsht_last_error().decode())
+    return out.T
 
 
 def legendre_table(m, x, degrees):

@@ -253,17 +253,18 @@ def _empty_stats():
 
 
 def plan_alt(n, m, params=None, n0=N0_DEFAULT, tau=TAU_DEFAULT,
-             quadrature=None, workers=1):
+             quadrature=None, workers=1, device=None):
     """Compressed two-parity plan for order m at half-size n
     (alt.py:85-152).
 
     BLAS/LAPACK run single-threaded inside: a threaded reduction could
-    change the last bits of a QR and with them the factors."""
+    change the last bits of a QR and with them the factors.  ``device``
+    (CUDA ordinal) tabulates the entries on that GPU (same bits)."""
     with threadpool_limits(limits=1):
-        return _plan_alt(n, m, params, n0, tau, quadrature, workers)
+        return _plan_alt(n, m, params, n0, tau, quadrature, workers, device)
 
 
-def _plan_alt(n, m, params, n0, tau, quadrature, workers):
+def _plan_alt(n, m, params, n0, tau, quadrature, workers, device=None):
     if not 0 <= m <= 2 * n - 1:
         raise ValueError(f"order {m} outside [0, {2 * n - 1}]")
     if params is None:
@@ -279,7 +280,7 @@ def _plan_alt(n, m, params, n0, tau, quadrature, workers):
             continue
         t0 = time.perf_counter()
         spec = make_alt_spec(n, m, parity, quadrature)
-        table = half_table(m, spec.offset, spec.x_pos, spec.num_cols)
+        table = half_table(m, spec.offset, spec.x_pos, spec.num_cols, device)
         leaves, deepest = partition(spec, n0)
         stats["levels_used"] = max(stats["levels_used"], deepest)
         kept, dropped = [], 0
@@ -379,16 +380,22 @@ def _map_payloads(plans, fn):
 
 
 def _plan_orders(args):
-    n, orders, params, n0, tau, spill = args
+    n, orders, params, n0, tau, spill, device = args
     quadrature = gauss_legendre(2 * n)
     out = []
+    trace = os.environ.get("BFSHT_PLAN_TRACE")
     for m in orders:
+        t0 = time.perf_counter()
         try:
             out.append(plan_alt(n, m, params, n0=n0, tau=tau,
-                                quadrature=quadrature))
+                                quadrature=quadrature, device=device))
         except Exception as exc:
             raise RuntimeError(f"planning failed at order m={m}: {exc}") \
                 from exc
+        if trace:
+            import sys
+            print(f"[plan pid {os.getpid()}] m={m} {time.perf_counter() - t0:.2f}s",
+                  file=sys.stderr, flush=True)
     if spill is None:
         return out, None
     # ship payloads through a shared file instead of the result pipe: the
@@ -420,6 +427,9 @@ def _start_method():
     """fork is cheapest, but forking a process whose CUDA / NCCL threads are
     running can deadlock the child: use forkserver once CUDA is up."""
     import sys
+    from . import legendre
+    if legendre.device_tables_used():
+        return "forkserver"   # this process holds a CUDA context (f3 tables)
     torch = sys.modules.get("torch")
     try:
         if torch is not None and torch.cuda.is_initialized():
@@ -430,10 +440,11 @@ def _start_method():
 
 
 def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
-                processes=1, quadrature=None):
+                processes=1, quadrature=None, device=None):
     """Plans for an arbitrary list of orders (one shard of an SHT), built in
     ``processes`` host processes (0/None = all cores); orders are dealt
-    round-robin, which balances cost because it falls with m."""
+    round-robin, which balances cost because it falls with m.  ``device``:
+    tabulate matrix entries on that GPU (f3; the factors are unchanged)."""
     orders = [int(m) for m in orders]
     if params is None:
         params = SamplingConfig()
@@ -448,7 +459,7 @@ def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
         for m in orders:
             try:
                 plans.append(plan_alt(n, m, params, n0=n0, tau=tau,
-                                      quadrature=quadrature))
+                                      quadrature=quadrature, device=device))
             except Exception as exc:
                 raise RuntimeError(
                     f"planning failed at order m={m}: {exc}") from exc
@@ -459,7 +470,7 @@ def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
     spill = _spill_dir()
     with ctx.Pool(p) as pool:
         res = pool.map(_plan_orders,
-                       [(n, c, params, n0, tau, spill) for c in chunks])
+                       [(n, c, params, n0, tau, spill, device) for c in chunks])
     by_m = {}
     for chunk, (got, path) in zip(chunks, res):
         if path is not None:
@@ -481,15 +492,15 @@ def plan_orders(n, orders, params=None, n0=None, tau=TAU_DEFAULT,
     return [by_m[m] for m in orders]
 
 
-def plan_sht(n, params=None, n0=None, tau=TAU_DEFAULT, processes=1):
+def plan_sht(n, params=None, n0=None, tau=TAU_DEFAULT, processes=1, device=None):
     """Plans for every order m = 0..2N-1 sharing one quadrature rule
     (sht.py:109-128).  ``processes > 1`` plans orders in parallel host
-    processes."""
+    processes; ``device`` tabulates entries on that GPU."""
     if n < 1:
         raise ValueError("n must be >= 1")
     if params is None:
         params = SamplingConfig()
     if processes is not None and processes > 1 and n < 8:
         processes = 1
-    plans = plan_orders(n, range(2 * n), params, n0, tau, processes)
+    plans = plan_orders(n, range(2 * n), params, n0, tau, processes, device=device)
     return ShtPlan(n=n, alt_plans=plans, params=params)

@@ -58,7 +58,8 @@ def test_idbf_apply_2d(k, cplx):
     assert rel(idbf_apply_transpose(fac, y), OA.idbf_apply_transpose(fac, y)) < 1e-14
 
 
-@pytest.mark.parametrize("n,m,nf", [(64, 0, 3), (64, 5, 8), (128, 40, 13), (256, 300, 1)])
+@pytest.mark.parametrize("n,m,nf", [(64, 0, 3), (64, 5, 8), (128, 40, 13), (256, 300, 1),
+                                       (128, 3, 40), (64, 1, 64)])
 def test_alt_fields_vs_oracle(n, m, nf):
     from paper_2004_11346_b200.api import alt_forward, alt_inverse
     plan = plan_alt(n, m, SamplingConfig(tolerance=1e-12), n0=64)
