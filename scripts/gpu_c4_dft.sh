@@ -2,10 +2,10 @@
 mkdir -p gpurun_out
 python -m paper_2004_11346_b200.build > gpurun_out/build.log 2>&1 || tail -5 gpurun_out/build.log
 timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_fields.py tests/test_gpu_sht.py tests/test_gpu_c2_parity.py tests/test_gpu_dft_big.py tests/test_gpu_pipeline.py tests/test_gpu_sharded.py tests/test_gpu_ooc.py 2>&1 | tail -3
-for v in row cluster legacy; do
+for v in cluster row legacy; do
   unset BFSHT_DFT_LEGACY BFSHT_DFT_SYNTH
   [ $v = legacy ] && export BFSHT_DFT_LEGACY=1
-  [ $v = cluster ] && export BFSHT_DFT_SYNTH=cluster
+  [ $v = row ] && export BFSHT_DFT_SYNTH=row
   echo "== $v"; timeout 600 python scripts/dft_stage_times.py --n ${DFT_NS:-1024,2048,4096} 2>&1 | grep '"kernel"' | python -c "
 import sys,json
 for l in sys.stdin:
