@@ -381,8 +381,72 @@ __device__ __forceinline__ void regen_chains(const double *sb, const double *__r
 // same number.  The step coefficients were staged into the slot at issue
 // time (cp.async, regen_coef) and are read as warp-uniform shared loads.
 // Padding rows / columns come out as zeros.
+// Emission of one column (e fixed for the block), as regen_block.
+__device__ __forceinline__ double regen_emit(double pc, long long thr, long long e52) {
+    return abits(pc) >= thr ? __longlong_as_double(__double_as_longlong(pc) + e52) : 0.0;
+}
+
+// Full 32 x 32 tile (the common case: turning blocks cut on the absolute
+// 32-grid): the same operation sequence as regen_chains<2> — chain h covers
+// columns 16h .. 16h+15, emit, two steps after every column but the chain's
+// last, range test after every 4 columns — as straight-line code: no
+// per-column edge tests, the two chains interleaved step by step for ILP,
+// and each block's 16 coefficient pairs loaded before its chain work.
+__device__ __forceinline__ void regen_full(const double *__restrict__ xpos, long long mag_bits,
+                                           double *T, int lane) {
+    constexpr int C4 = 8, R = 32;
+    const int r_a = __double2loint(T[0]);
+    double pp0 = T[2 + 3 * lane], pc0 = T[3 + 3 * lane];
+    int e0 = (int)T[4 + 3 * lane];
+    double pp1 = T[2 + 3 * (R + lane)], pc1 = T[3 + 3 * (R + lane)];
+    int e1 = (int)T[4 + 3 * (R + lane)];
+    const double x = __ldg(xpos + r_a + lane);
+    __syncwarp();   // seeds read: their slot region may now be overwritten
+    double *row = T + (lane >> 2) * C4 * 16 + (lane & 3) * 4;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        double2 c0[8], c1[8];
+        const double2 *b0 = reinterpret_cast<const double2 *>(T + regen_coef(4 * j, C4));
+        const double2 *b1 = reinterpret_cast<const double2 *>(T + regen_coef(16 + 4 * j, C4));
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            c0[t] = b0[t];
+            c1[t] = b1[t];
+        }
+        const long long e52a = (long long)e0 << 52, e52b = (long long)e1 << 52;
+        const long long tha = e0 <= -1700 ? 0x7fffffffffffffffLL : mag_bits - e52a;
+        const long long thb = e1 <= -1700 ? 0x7fffffffffffffffLL : mag_bits - e52b;
+        double v0[4], v1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            v0[i] = regen_emit(pc0, tha, e52a);
+            v1[i] = regen_emit(pc1, thb, e52b);
+            if (j < 3 || i < 3) {
+                rec_step(x, c0[2 * i].x, c0[2 * i].y, pp0, pc0);
+                rec_step(x, c1[2 * i].x, c1[2 * i].y, pp1, pc1);
+                rec_step(x, c0[2 * i + 1].x, c0[2 * i + 1].y, pp0, pc0);
+                rec_step(x, c1[2 * i + 1].x, c1[2 * i + 1].y, pp1, pc1);
+            }
+        }
+        rec_rescale(pp0, pc0, e0);
+        rec_rescale(pp1, pc1, e1);
+        __syncwarp();   // every lane has read this block's coefficients
+        double2 *d0 = reinterpret_cast<double2 *>(row + j * 16);
+        double2 *d1 = reinterpret_cast<double2 *>(row + (4 + j) * 16);
+        d0[0] = make_double2(v0[0], v0[1]);
+        d0[1] = make_double2(v0[2], v0[3]);
+        d1[0] = make_double2(v1[0], v1[1]);
+        d1[1] = make_double2(v1[2], v1[3]);
+    }
+    __syncwarp();
+}
+
 __device__ __noinline__ void regen_tile(const double *__restrict__ xpos, long long mag_bits, int R,
                                         int C, double *T, int lane) {
+    if (R == BF_T && C == BF_T) {
+        regen_full(xpos, mag_bits, T, lane);
+        return;
+    }
     if (bf_seed_chains(C) == 2)
         regen_chains<2>(T, xpos, mag_bits, R, C, T, lane);
     else
