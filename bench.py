@@ -158,7 +158,7 @@ def measured_traffic(n, world, regen):
     committed ncu launch list of this command (profiles/), for the same
     workload only; None otherwise."""
     try:
-        with open(os.path.join(ROOT, "profiles", f"r01_traffic_n{n}.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", f"r02_traffic_n{n}.json")) as fh:
             t = json.load(fh)
     except (OSError, ValueError):
         return None
