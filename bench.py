@@ -168,34 +168,65 @@ def measured_traffic(n, world, regen):
 
 
 # ----------------------------------------------------------- reference arm
+# Every host core is a worker process holding the plans of a round-robin
+# share of |m| (the reference planner's factors, built in the worker).  The
+# step's arrays live in shared memory (/dev/shm): the coefficients, the
+# binned forward spectrum, the grid, the inverse spectrum and the output
+# coefficients, so nothing but a phase number crosses the process pipes.
+# Phases per step: (1) forward ALT of the worker's orders into the binned
+# spectrum columns (sht.py:143-147); (2) a contiguous range of colatitude
+# rows: grid = L ifft(row) (sht.py:148), then the inverse's spectrum
+# fft(grid row) / L (sht.py:161); (3) inverse ALT of the worker's orders
+# from the spectrum columns (sht.py:162-165).  This is oracle/apply.py's
+# sht_forward + sht_inverse (the reference algorithm) split over processes.
 _REF_STATE = {}
 
 
-def _ref_worker_init(n, orders, tol):
+def _ref_attach(specs):
+    from multiprocessing import shared_memory
+    arrs, keep = {}, []
+    for name, (shm_name, shape) in specs.items():
+        shm = shared_memory.SharedMemory(name=shm_name)
+        keep.append(shm)
+        arrs[name] = np.ndarray(shape, dtype=np.complex128, buffer=shm.buf)
+    return arrs, keep
+
+
+def _ref_worker_init(n, orders, rows, tol, specs):
     from paper_2004_11346_b200 import SamplingConfig, plan_orders
     os.environ["OMP_NUM_THREADS"] = "1"
     plans = plan_orders(n, orders, SamplingConfig(tolerance=tol), processes=1)
     _REF_STATE["plans"] = {p.m: p for p in plans}
+    _REF_STATE["rows"] = rows
+    _REF_STATE["n"] = n
+    _REF_STATE["arr"], _REF_STATE["keep"] = _ref_attach(specs)
 
 
-def _ref_worker_forward(job):
+def _ref_worker_phase(phase):
     import oracle.apply as OA
     from threadpoolctl import threadpool_limits
-    out = {}
+    st = _REF_STATE
+    n, arr = st["n"], st["arr"]
+    num_phi, ms, bns = OA.bins(n)
+    _, offs = OA.coeff_offsets(n)
+    phi0 = np.pi / num_phi
     with threadpool_limits(limits=1):
-        for m, vec in job:
-            out[m] = OA.alt_forward(_REF_STATE["plans"][abs(m)], vec)
-    return out
-
-
-def _ref_worker_inverse(job):
-    import oracle.apply as OA
-    from threadpoolctl import threadpool_limits
-    out = {}
-    with threadpool_limits(limits=1):
-        for m, col in job:
-            out[m] = OA.alt_inverse(_REF_STATE["plans"][abs(m)], col)
-    return out
+        if phase == 1:
+            for i, (m, b) in enumerate(zip(ms, bns)):
+                if abs(int(m)) in st["plans"]:
+                    g = OA.alt_forward(st["plans"][abs(int(m))], arr["coeff"][offs[i]:offs[i + 1]])
+                    arr["buf"][:, b] = g * np.exp(1j * m * phi0)
+        elif phase == 2:
+            r0, r1 = st["rows"]
+            if r1 > r0:
+                arr["grid"][r0:r1] = num_phi * np.fft.ifft(arr["buf"][r0:r1], axis=1)
+                arr["spec"][r0:r1] = np.fft.fft(arr["grid"][r0:r1], axis=1) / num_phi
+        else:
+            for i, (m, b) in enumerate(zip(ms, bns)):
+                if abs(int(m)) in st["plans"]:
+                    g = arr["spec"][:, b] * np.exp(-1j * m * phi0)
+                    arr["out"][offs[i]:offs[i + 1]] = OA.alt_inverse(st["plans"][abs(int(m))], g)
+    return phase
 
 
 def _ref_worker_ready(_):
@@ -205,6 +236,7 @@ def _ref_worker_ready(_):
 def run_reference(args):
     """CPU arm: the reference algorithm (oracle port) on every host core."""
     import multiprocessing as mp
+    from multiprocessing import shared_memory
     import oracle.apply as OA
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -212,55 +244,57 @@ def run_reference(args):
         return 0
     n = args.n
     cores = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    # every core plans and owns a round-robin share of |m|
-    shards = [list(range(r, 2 * n, cores)) for r in range(cores)]
-    pools = [ctx.Pool(1, initializer=_ref_worker_init, initargs=(n, s, args.tol))
-             for s in shards]
-    t0 = time.time()
-    for p in pools:
-        p.apply(_ref_worker_ready, (0,))
-    t_plan = time.time() - t0
+    num_phi, _, _ = OA.bins(n)
+    _, offs = OA.coeff_offsets(n)
+    shapes = {"coeff": (int(offs[-1]),), "buf": (2 * n, num_phi), "grid": (2 * n, num_phi),
+              "spec": (2 * n, num_phi), "out": (int(offs[-1]),)}
+    shms, specs, arr = [], {}, {}
+    for name, shape in shapes.items():
+        shm = shared_memory.SharedMemory(create=True, size=int(np.prod(shape)) * 16)
+        shms.append(shm)
+        specs[name] = (shm.name, shape)
+        arr[name] = np.ndarray(shape, dtype=np.complex128, buffer=shm.buf)
     flat = synthetic_coeffs(n)
-    ms, offs = OA.coeff_offsets(n)
-    num_phi, _, bins = OA.bins(n)
-    phi0 = np.pi / num_phi
+    arr["coeff"][:] = flat
+    arr["buf"][:] = 0
+    ctx = mp.get_context("fork")
+    # every core plans and owns a round-robin share of |m| and a row range
+    shards = [list(range(r, 2 * n, cores)) for r in range(cores)]
+    edges = [(2 * n * r) // cores for r in range(cores + 1)]
+    pools = [ctx.Pool(1, initializer=_ref_worker_init,
+                      initargs=(n, s, (edges[r], edges[r + 1]), args.tol, specs))
+             for r, s in enumerate(shards)]
+    try:
+        t0 = time.time()
+        for p in pools:
+            p.apply(_ref_worker_ready, (0,))
+        t_plan = time.time() - t0
 
-    def step():
-        jobs = [[] for _ in shards]
-        for i, m in enumerate(ms):
-            jobs[abs(m) % cores].append((int(m), flat[offs[i]:offs[i + 1]]))
-        res = [p.apply_async(_ref_worker_forward, (j,)) for p, j in zip(pools, jobs)]
-        buf = np.zeros((2 * n, num_phi), dtype=np.complex128)
-        for r in res:
-            for m, g in r.get().items():
-                buf[:, m % num_phi] = g * np.exp(1j * m * phi0)
-        grid = num_phi * np.fft.ifft(buf, axis=1)
-        spectrum = np.fft.fft(grid, axis=1) / num_phi
-        jobs = [[] for _ in shards]
-        for m in ms:
-            g = spectrum[:, m % num_phi] * np.exp(-1j * m * phi0)
-            jobs[abs(m) % cores].append((int(m), g))
-        res = [p.apply_async(_ref_worker_inverse, (j,)) for p, j in zip(pools, jobs)]
-        out = np.zeros(offs[-1], dtype=np.complex128)
-        for r in res:
-            for m, b in r.get().items():
-                i = m + 2 * n - 1
-                out[offs[i]:offs[i + 1]] = b
-        return out
+        def step():
+            for phase in (1, 2, 3):
+                res = [p.apply_async(_ref_worker_phase, (phase,)) for p in pools]
+                for r in res:
+                    r.get()
+            return arr["out"]
 
-    for _ in range(args.warmup):
-        step()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        step()
-    dt = time.perf_counter() - t0
-    for p in pools:
-        p.terminate()
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            step()
+        dt = time.perf_counter() - t0
+        rt = float(np.linalg.norm(arr["out"] - flat) / np.linalg.norm(flat))
+    finally:
+        for p in pools:
+            p.terminate()
+        for shm in shms:
+            shm.close()
+            shm.unlink()
     value = args.steps / dt
-    sample = (f"full N={n} SHT fwd+inv per step, {cores} processes "
-              f"(one per host core, orders dealt round-robin, numpy FFT in "
-              f"parent); planning {t_plan:.1f}s excluded")
+    sample = (f"full N={n} SHT fwd+inv per step, {cores} processes (one per "
+              f"host core: orders dealt round-robin, phi FFTs on row ranges, "
+              f"arrays in shared memory); planning {t_plan:.1f}s excluded; "
+              f"round trip {rt:.2e}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
