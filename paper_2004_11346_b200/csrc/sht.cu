@@ -111,8 +111,17 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
 #pragma unroll
         for (int q = 0; q < P; ++q) x[q] = row[base + q * span];
         if (!DIF && span > 1) {
+            // w^q as powers of the one loaded w (table entry q = 1): one
+            // twiddle load per butterfly instead of P - 1 (the passes are
+            // L1-bound); <= P - 2 extra roundings, ~1e-15 relative
+            const double2 w1 = conjif(Tw[k], inv);
+            double2 w = w1;
+            x[1] = cmul(x[1], w);
 #pragma unroll
-            for (int q = 1; q < P; ++q) x[q] = cmul(x[q], conjif(Tw[(q - 1) * span + k], inv));
+            for (int q = 2; q < P; ++q) {
+                w = cmul(w, w1);
+                x[q] = cmul(x[q], w);
+            }
         }
         double2 y[P];
         if (P == 2) {
@@ -159,8 +168,14 @@ __device__ __forceinline__ void radix_pass(double2 *buf, int nrows, int L, int s
             }
         }
         if (DIF && span > 1) {
+            const double2 w1 = conjif(Tw[k], inv);
+            double2 w = w1;
+            y[1] = cmul(y[1], w);
 #pragma unroll
-            for (int q = 1; q < P; ++q) y[q] = cmul(y[q], conjif(Tw[(q - 1) * span + k], inv));
+            for (int q = 2; q < P; ++q) {
+                w = cmul(w, w1);
+                y[q] = cmul(y[q], w);
+            }
         }
 #pragma unroll
         for (int q = 0; q < P; ++q) row[base + q * span] = y[q];
