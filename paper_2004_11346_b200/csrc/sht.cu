@@ -360,6 +360,7 @@ __device__ void dft_passes(double2 *buf, int nrows, const DftDesc &d, const doub
             case 4: radix_pass<4>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 5: radix_pass<5>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 7: radix_pass<7>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 9: radix_pass<9>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 11: radix_pass<11>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 13: radix_pass<13>(buf, nrows, L, span, si, tw, rr, inv); break;
             default:
@@ -387,6 +388,7 @@ __device__ void dft_passes_dif(double2 *buf, int nrows, const DftDesc &d, const 
             case 4: radix_pass<4, true>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 5: radix_pass<5, true>(buf, nrows, L, span, si, tw, rr, inv); break;
             case 7: radix_pass<7, true>(buf, nrows, L, span, si, tw, rr, inv); break;
+            case 9: radix_pass<9, true>(buf, nrows, L, span, si, tw, rr, inv); break;
             default: __trap();
         }
         __syncthreads();
@@ -1187,7 +1189,16 @@ std::vector<int> factorize(int64_t L) {
     }
     for (; twos >= 2; twos -= 2) f.push_back(4);
     if (twos) f.push_back(2);
-    for (int p = 3; (int64_t)p * p <= L; p += 2)
+    // pairs of 3s as one radix-9 pass (one shared-memory round trip fewer;
+    // the passes are L1-bound)
+    int threes = 0;
+    while (L % 3 == 0) {
+        ++threes;
+        L /= 3;
+    }
+    for (; threes >= 2; threes -= 2) f.push_back(9);
+    if (threes) f.push_back(3);
+    for (int p = 5; (int64_t)p * p <= L; p += 2)
         while (L % p == 0) {
             f.push_back(p);
             L /= p;
