@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--force-sharded", action="store_true",
                     help="run the multi-GPU (order-sharded, NCCL) runner even at one "
                          "rank: exercises the scaling path of this script on one GPU")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the timed steps directly instead of replaying a CUDA graph")
     ap.add_argument("--plan-cache", default="",
                     help="directory of packed per-rank plans (BFPK files): loaded when "
                          "present, written otherwise (skips planning on later runs)")
@@ -433,6 +435,15 @@ def run_ours(args):
         runner.forward(coeffs, grid)
         runner.inverse(grid, back)
 
+    # one GPU: the step replays as a CUDA graph (same kernels, same work;
+    # no per-launch host overhead or inter-launch gaps)
+    graph, launches_per_step = None, None
+    if not sharded and not args.no_graph:
+        graph, launches_per_step = runner.capture_step(coeffs, grid, back)
+
+        def step():  # noqa: F811
+            graph.replay()
+
     def barrier():
         if world > 1:
             torch.distributed.barrier()
@@ -454,6 +465,8 @@ def run_ours(args):
     ev1.record()
     barrier()
     launches = runner.launches_total() - launches0
+    if graph is not None:
+        launches = launches_per_step * args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop()
     if world > 1:

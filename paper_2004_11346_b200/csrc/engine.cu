@@ -1051,6 +1051,7 @@ int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) 
     }
     int rc = bf_ensure_smem((const void *)alt_group_kernel, (int)kGroupSmem);
     if (rc) return rc;
+    BF_CUDA(cudaMemsetAsync(pl->counters, 0, sizeof(int) * nst, st));
     for (int s = 0; s < nst; ++s) {
         if (b[s + 1] <= b[s]) continue;
         StageArgs a;
@@ -1066,7 +1067,6 @@ int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) 
         a.rec = pl->rec;
         a.xpos = pl->xpos;
         std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
-        BF_CUDA(cudaMemsetAsync(a.counter, 0, sizeof(int), st));
         const int64_t want = (a.ntasks + kGroups - 1) / kGroups;
         const int grid = (int)(want < pl->sm_count ? want : pl->sm_count);
         alt_group_kernel<<<grid, kGroups * kGW * 32, kGroupSmem, st>>>(a);
@@ -1076,9 +1076,11 @@ int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) 
     return 0;
 }
 
+// reset: zero the stage's task counter first (single-stage calls); the
+// whole-direction paths zero every stage counter with one memset instead
 template <int NR>
 static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, double *arena,
-                        cudaStream_t st, int max_ctas) {
+                        cudaStream_t st, int max_ctas, bool reset) {
     constexpr int W = Width<NR>::WARPS;
     const size_t smem = sizeof(WarpRing<NR>) * W;
     int rc = bf_ensure_smem((const void *)alt_stage_kernel<NR>, (int)smem);
@@ -1096,7 +1098,7 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
     a.rec = pl->rec;
     a.xpos = pl->xpos;
     std::memcpy(&a.mag_min, &pl->info[22], sizeof(double));
-    BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    if (reset) BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     int64_t want = (a.ntasks + W - 1) / W;
     const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;
     int grid = (int)(want < cap ? want : cap);
@@ -1109,7 +1111,7 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
 int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st,
                  int max_ctas) {
     if (t1 <= t0) return 0;
-    return launch_stage<BF_NRHS>(pl, t0, t1, counter, pl->arena, st, max_ctas);
+    return launch_stage<BF_NRHS>(pl, t0, t1, counter, pl->arena, st, max_ctas, true);
 }
 
 // All stages of one direction over a wide (16 RHS per entry) arena.
@@ -1120,9 +1122,11 @@ int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) {
         bfsht_set_error("plan counters not allocated");
         return -3;
     }
+    BF_CUDA(cudaMemsetAsync(pl->counters, 0, sizeof(int) * nst, st));
     for (int s = 0; s < nst; ++s) {
         if (b[s + 1] <= b[s]) continue;
-        int rc = launch_stage<BF_WIDE_NRHS>(pl, b[s], b[s + 1], pl->counters + s, arena, st, 0);
+        int rc =
+            launch_stage<BF_WIDE_NRHS>(pl, b[s], b[s + 1], pl->counters + s, arena, st, 0, false);
         if (rc) return rc;
     }
     return 0;
@@ -1135,8 +1139,11 @@ int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t st) {
         bfsht_set_error("plan counters not allocated");
         return -3;
     }
+    BF_CUDA(cudaMemsetAsync(pl->counters, 0, sizeof(int) * nst, st));
     for (int s = 0; s < nst; ++s) {
-        int rc = bf_run_stage(pl, b[s], b[s + 1], pl->counters + s, st, 0);
+        if (b[s + 1] <= b[s]) continue;
+        int rc = launch_stage<BF_NRHS>(pl, b[s], b[s + 1], pl->counters + s, pl->arena, st, 0,
+                                       false);
         if (rc) return rc;
     }
     return 0;

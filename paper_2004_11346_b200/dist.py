@@ -251,6 +251,27 @@ class SingleRunner(_Common):
         else:
             self.dp.sht_inverse(grid, coeffs)
 
+    def capture_step(self, coeffs, grid, back):
+        """One forward + inverse on fixed device buffers as a CUDA graph:
+        the ~35 launches and counter resets of a step replay without
+        per-launch host work or stream gaps.  Returns (graph, launches
+        per step).  The step is run once outside capture first, so every
+        lazily built table and kernel attribute exists before capture."""
+        import torch
+        side = torch.cuda.Stream(self.dp.device)
+        side.wait_stream(torch.cuda.current_stream(self.dp.device))
+        with torch.cuda.stream(side):
+            self.forward(coeffs, grid)
+            self.inverse(grid, back)
+        torch.cuda.current_stream(self.dp.device).wait_stream(side)
+        torch.cuda.synchronize(self.dp.device)
+        graph = torch.cuda.CUDAGraph()
+        l0 = self.launches_total()
+        with torch.cuda.graph(graph):
+            self.forward(coeffs, grid)
+            self.inverse(grid, back)
+        return graph, self.launches_total() - l0
+
     def alt_bytes(self):
         if self.batch == 1:
             return _Common.alt_bytes(self)
