@@ -352,8 +352,32 @@ class _ArrRef:
         self.off, self.shape, self.dtype = off, shape, dtype
 
 
+def _reap_spills(d):
+    """Remove spill files of planner workers that no longer exist (a run
+    killed between a worker's write and the parent's unlink leaves its
+    payload file behind in tmpfs)."""
+    try:
+        names = os.listdir(d)
+    except OSError:
+        return
+    for name in names:
+        if not (name.startswith("bfsht_plan_") and name.endswith(".bin")):
+            continue
+        try:
+            pid = int(name.split("_")[2])
+            os.kill(pid, 0)
+        except ProcessLookupError:
+            try:
+                os.unlink(os.path.join(d, name))
+            except OSError:
+                pass
+        except (ValueError, IndexError, PermissionError):
+            pass
+
+
 def _spill_dir():
     # tmpfs when it has room for the payloads, else the regular temp dir
+    _reap_spills("/dev/shm")
     try:
         st = os.statvfs("/dev/shm")
         if st.f_bavail * st.f_frsize > (8 << 30):
