@@ -96,7 +96,7 @@ class ChunkedSht:
 
     def __init__(self, n, nchunks, params=None, tau=None, n0=None, processes=0,
                  planner=None, reserve_bytes=24 << 30, device=None, verbose=False,
-                 only=None):
+                 only=None, regen=0.0):
         import torch
         from .api import DevicePlan
         from .legendre import gauss_legendre
@@ -114,6 +114,10 @@ class ChunkedSht:
                                    processes=processes, quadrature=self.quadrature)
         self.planner = planner
         self.reserve_bytes = int(reserve_bytes)
+        # regen: fraction of full-height turning tiles stored as recurrence
+        # seeds and regenerated on the GPU (§8 f1): ~4.7x fewer bytes for
+        # those tiles, so more chunks stay resident between directions
+        self.regen = float(regen)
         self.verbose = verbose
         # only: chunk indices to process (None = all).  A subset runs the
         # full-size grid and DFT stage with the other orders' node halves
@@ -151,7 +155,7 @@ class ChunkedSht:
         t0 = time.perf_counter()
         plans = self.planner(self.chunks[c])
         t1 = time.perf_counter()
-        dp = DevicePlan(plans, weights=self.quadrature.weights)
+        dp = DevicePlan(plans, weights=self.quadrature.weights, regen=self.regen)
         del plans
         self.torch.cuda.synchronize()
         # the device copy is all that is needed from here: drop the host
@@ -252,6 +256,8 @@ class ChunkedSht:
                       f"{(total - free) / 1e9:.1f} GB", file=sys.stderr, flush=True)
             del dp, coeffs
             torch.cuda.empty_cache()
+        free, total = torch.cuda.mem_get_info(self.device)
+        rep["gpu_mem_used_gb"] = (total - free) / 1e9
         st = self._stream()
         self._timed("dft", lambda: check(lib, lib.bfsht_synth_rows(
             self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, n, _ptr(grid), st),

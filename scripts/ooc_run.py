@@ -50,6 +50,9 @@ def main():
                          "is planned (forward, and inverse on a pocketfft spectrum of the "
                          "GPU grid); implies no resident chunks (all replanned)")
     ap.add_argument("--oracle-threads", type=int, default=0)
+    ap.add_argument("--regen", type=float, default=0.0,
+                    help="fraction of full-height turning tiles regenerated on the GPU "
+                         "(f1): smaller resident chunks")
     args = ap.parse_args()
 
     import torch
@@ -112,7 +115,7 @@ def main():
         flat = synthetic_coeffs(n, seed=3)
     run = ChunkedSht(n, args.chunks, params=params, processes=args.procs,
                      reserve_bytes=int(args.reserve_gb * (1 << 30)), verbose=True, only=only,
-                     planner=planner)
+                     planner=planner, regen=args.regen)
     if args.oracle_all:
         # the context plan (order 2N-1) went through the planner too
         ora["fwd_buf"][:] = 0.0
@@ -304,6 +307,7 @@ def main():
 
     v_n = fwd["payload_values"]
     dev_ms = fwd["device_ms"] + inv["device_ms"]
+    resident = [c for c in fwd["chunks"] if c.get("resident")]
     res = {
         "workload": f"C3: SHT fwd+inv N={n}, tol {args.tol:g}, one B200, orders in "
                     f"{len(run.chunks)} chunks (plan > HBM: planned/packed/uploaded per chunk)",
@@ -322,6 +326,10 @@ def main():
         "checks": checks,
         "samples": samples,
         "alt_ms_per_chunk_fwd": fwd["alt_ms_per_chunk"],
+        "regen": args.regen,
+        "resident_chunks_after_forward": len(resident),
+        "resident_tile_gb": sum(c.get("tile_gb", 0.0) for c in resident),
+        "gpu_mem_used_gb_after_forward": fwd.get("gpu_mem_used_gb"),
     }
     if only is not None:
         res["workload"] = (f"C5-style sampled run: N={n}, tol {args.tol:g}, one B200, chunks {only} "
