@@ -461,296 +461,12 @@ __global__ void __launch_bounds__(kDftThreads, 2) dft_rows_kernel(
     }
 }
 
-// ---- forward SHT: node halves -> assembled rows -> L*ifft -> grid rows
-template <bool SM>
-__global__ void __launch_bounds__(kDftThreads) sht_synth_kernel(
-    DftDesc d, int n, const bf_half *__restrict__ halves, const double *__restrict__ arena,
-    int r_begin, int r_count, const double2 *__restrict__ tw, const int *__restrict__ perm,
-    const double2 *__restrict__ W, double2 *__restrict__ grid, bool use_smem,
-    double2 *scratch, bool w_smem, int64_t yr, int ystride, int ew,
-    const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
-    // ystride > 0 (whole-SHT path): entry (order am, parity p, row rr) sits
-    // at yr + rr * ystride + 2 am + p in the row-major node array Yr, and
-    // absent halves read as zeros there (never written), so no layout-table
-    // lookup stands between a bin and its loads.  Otherwise:
-    // node-half entries of row pair r live at halves[.].y + (r - r_begin);
-    // grid holds 2*r_count local rows: lower rows n-r_begin-r_count .. n-r_begin-1
-    // then upper rows n+r_begin .. n+r_begin+r_count-1 (the full grid when
-    // r_begin = 0, r_count = n)
-    const int L = d.L, Lb = d.Lb;
-    double2 *buf = dft_buffer<SM>(scratch, 2, Lb);
-    // twiddle table next to the rows in shared memory when it fits
-    const double2 *Wt = W;
-    if (SM && w_smem) {
-        double2 *ws = buf + 2 * Lb;
-        for (int i = threadIdx.x; i < Lb; i += blockDim.x) ws[i] = W[i];
-        __syncthreads();
-        Wt = ws;
-    }
-    const int mtop = 2 * n - 1;
-    for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
-    const int rr = r - r_begin;
-    row_clear(buf, 2, d);
-    // one thread per order |m|: its odd and even node-half entries (+m and
-    // -m, 32 B each, adjacent in Yr) are read whole and feed the two bins
-    // m and L-m of both rows, so every loaded sector is fully used; orders
-    // in batches of kBatch per thread, every load of a batch issued before
-    // any is used (otherwise a chain of dependent DRAM latencies)
-    constexpr int kBatch = 4;
-    const int nord = mtop + 1;
-    for (int a0 = threadIdx.x; a0 < nord; a0 += kBatch * blockDim.x) {
-        double2 op[kBatch], on[kBatch], ep[kBatch], en[kBatch], tp[kBatch], tn[kBatch];
-        int pp[kBatch], pn[kBatch];
-        if (ystride > 0) {
-            const double *rowp = arena + (yr + (int64_t)rr * ystride) * ew;
-#pragma unroll
-            for (int i = 0; i < kBatch; ++i) {
-                const int am = a0 + i * blockDim.x;
-                const bool ok = am < nord;
-                op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
-                if (ok) {
-                    const double2 *eo = reinterpret_cast<const double2 *>(rowp + (2 * am) * ew);
-                    const double2 *ee = reinterpret_cast<const double2 *>(rowp + (2 * am + 1) * ew);
-                    op[i] = eo[0];
-                    on[i] = eo[1];
-                    ep[i] = ee[0];
-                    en[i] = ee[1];
-                }
-                const int bn = am > 0 ? L - am : 0;
-                tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
-                tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
-                if (d.blue && ok) {
-                    tp[i] = cmul(tp[i], conjif(chirp[am], true));
-                    tn[i] = cmul(tn[i], conjif(chirp[bn], true));
-                }
-                pp[i] = ok ? perm[am] : 0;
-                pn[i] = ok ? perm[bn] : 0;
-            }
-        } else {
-        bf_half ho[kBatch], he[kBatch];
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int am = a0 + i * blockDim.x < nord ? a0 + i * blockDim.x : 0;
-            ho[i] = halves[2 * am];
-            he[i] = halves[2 * am + 1];
-        }
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int am = a0 + i * blockDim.x;
-            const bool ok = am < nord;
-            op[i] = on[i] = ep[i] = en[i] = make_double2(0.0, 0.0);
-            if (ok && ho[i].ncols > 0) {
-                const double2 *eo = reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew);
-                op[i] = eo[0];
-                on[i] = eo[1];
-            }
-            if (ok && he[i].ncols > 0) {
-                const double2 *ee = reinterpret_cast<const double2 *>(
-                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew);
-                ep[i] = ee[0];
-                en[i] = ee[1];
-            }
-            const int bn = am > 0 && ok ? L - am : 0;
-            tp[i] = ok ? tw[am] : make_double2(0.0, 0.0);
-            tn[i] = ok ? tw[bn] : make_double2(0.0, 0.0);
-            if (d.blue && ok) {
-                tp[i] = cmul(tp[i], conjif(chirp[am], true));
-                tn[i] = cmul(tn[i], conjif(chirp[bn], true));
-            }
-            pp[i] = ok ? perm[am] : 0;
-            pn[i] = ok ? perm[bn] : 0;
-        }
-        }
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int am = a0 + i * blockDim.x;
-            if (am < nord) {
-                buf[pp[i]] = cmul(make_double2(ep[i].x + op[i].x, ep[i].y + op[i].y), tp[i]);
-                buf[Lb + pp[i]] = cmul(make_double2(ep[i].x - op[i].x, ep[i].y - op[i].y), tp[i]);
-                if (am > 0) {
-                    buf[pn[i]] = cmul(make_double2(en[i].x + on[i].x, en[i].y + on[i].y), tn[i]);
-                    buf[Lb + pn[i]] = cmul(make_double2(en[i].x - on[i].x, en[i].y - on[i].y), tn[i]);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    row_dft<true>(buf, 2, d, Wt, W + Lb, H, true);
-    double2 *up = grid + (int64_t)(r_count + rr) * L;
-    double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
-    // batched so several (scratch-path: L2) loads are in flight per thread
-    for (int j0 = threadIdx.x; j0 < L; j0 += 4 * blockDim.x) {
-        double2 vu[4], vl[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * blockDim.x;
-            if (j < L) {
-                const int pj = d.blue ? perm[j] : j;
-                vu[u] = buf[pj];
-                vl[u] = buf[Lb + pj];
-                if (d.blue) {
-                    const double2 c = conjif(chirp[j], true);
-                    vu[u] = cmul(vu[u], c);
-                    vl[u] = cmul(vl[u], c);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u * blockDim.x;
-            if (j < L) {
-                up[j] = vu[u];
-                lo[j] = vl[u];
-            }
-        }
-    }
-    __syncthreads();
-    }
-}
-
-// ---- inverse SHT: grid rows -> fft/L -> phase -> weighted fold -> node halves
-template <bool SM>
-__global__ void __launch_bounds__(kDftThreads) sht_anal_kernel(
-    DftDesc d, int n, const bf_half *__restrict__ halves, double *__restrict__ arena,
-    const double2 *__restrict__ tw, const int *__restrict__ perm,
-    const double2 *__restrict__ W, const double2 *__restrict__ grid,
-    const double *__restrict__ weights, int r_begin, int r_count, bool use_smem,
-    double2 *scratch, bool w_smem, const int *__restrict__ node_y, int ny, int ew,
-    const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
-    const int L = d.L, Lb = d.Lb;
-    double2 *buf = dft_buffer<SM>(scratch, 2, Lb);
-    // twiddle table next to the rows in shared memory when it fits
-    const double2 *Wt = W;
-    if (SM && w_smem) {
-        double2 *ws = buf + 2 * Lb;
-        for (int i = threadIdx.x; i < Lb; i += blockDim.x) ws[i] = W[i];
-        Wt = ws;
-    }
-    // whole-SHT path: node-half bases (-1 = absent half) staged in shared
-    // memory after the twiddles, replacing per-bin layout-table loads
-    int *ys = nullptr;
-    if (SM && w_smem && node_y) {
-        ys = reinterpret_cast<int *>(buf + 3 * Lb);
-        for (int i = threadIdx.x; i < ny; i += blockDim.x) ys[i] = node_y[i];
-    }
-    __syncthreads();
-    for (int r = r_begin + blockIdx.x; r < r_begin + r_count; r += gridDim.x) {
-    const int rr = r - r_begin;
-    const double2 *up = grid + (int64_t)(r_count + rr) * L;
-    const double2 *lo = grid + (int64_t)(r_count - 1 - rr) * L;
-    row_clear(buf, 2, d);
-    constexpr int kBatch = 8;   // issue a batch of loads before using any
-    for (int j0 = threadIdx.x; j0 < L; j0 += kBatch * blockDim.x) {
-        double2 u[kBatch], v[kBatch];
-        int p[kBatch];
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i) {
-            const int j = j0 + i * blockDim.x;
-            if (j < L) {
-                p[i] = perm[j];
-                u[i] = up[j];
-                v[i] = lo[j];
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kBatch; ++i)
-            if (j0 + i * blockDim.x < L) {
-                if (d.blue) {
-                    const double2 c = chirp[j0 + i * blockDim.x];
-                    u[i] = cmul(u[i], c);
-                    v[i] = cmul(v[i], c);
-                }
-                buf[p[i]] = u[i];
-                buf[Lb + p[i]] = v[i];
-            }
-    }
-    __syncthreads();
-    row_dft<true>(buf, 2, d, Wt, W + Lb, H, false);
-    const double w = weights[n + r];
-    const double invL = 1.0 / (double)L;
-    const int mtop = 2 * n - 1;
-    // one thread per order |m|: bins m and L-m of both rows give the +m and
-    // -m halves of its odd and even node-half entries, each written whole
-    // (32 B, full sectors) rather than as two 16-B halves at different times
-    const int nord = mtop + 1;
-    constexpr int kOut = 4;
-    for (int a0 = threadIdx.x; a0 < nord; a0 += kOut * blockDim.x) {
-        bf_half ho[kOut], he[kOut];
-        double2 tp[kOut], tn[kOut];
-#pragma unroll
-        for (int i = 0; i < kOut; ++i) {
-            const int am0 = a0 + i * blockDim.x;
-            const int am = am0 < nord ? am0 : 0;
-            if (ys) {
-                const int yo = ys[2 * am], ye = ys[2 * am + 1];
-                ho[i].y = yo;
-                ho[i].x = 1;
-                ho[i].ncols = yo >= 0;
-                he[i].y = ye;
-                he[i].x = 1;
-                he[i].ncols = ye >= 0;
-            } else {
-                ho[i] = halves[2 * am];
-                he[i] = halves[2 * am + 1];
-            }
-            tp[i] = tw[am];
-            tn[i] = tw[am > 0 ? L - am : 0];
-        }
-#pragma unroll
-        for (int i = 0; i < kOut; ++i) {
-            const int am = a0 + i * blockDim.x;
-            if (am >= nord) continue;
-            const int bn = L - am;
-            const int pa = d.blue ? perm[am] : am, pb = d.blue ? perm[bn] : bn;
-            double2 sa = buf[pa], sb = buf[Lb + pa];
-            if (d.blue) {
-                const double2 c = chirp[am];
-                sa = cmul(sa, c);
-                sb = cmul(sb, c);
-            }
-            const double2 cp = make_double2(tp[i].x, -tp[i].y);
-            sa = cmul(make_double2(sa.x * invL, sa.y * invL), cp);
-            sb = cmul(make_double2(sb.x * invL, sb.y * invL), cp);
-            double2 na = make_double2(0.0, 0.0), nb = na;
-            if (am > 0) {
-                const double2 cn = make_double2(tn[i].x, -tn[i].y);
-                na = buf[pb];
-                nb = buf[Lb + pb];
-                if (d.blue) {
-                    const double2 c = chirp[bn];
-                    na = cmul(na, c);
-                    nb = cmul(nb, c);
-                }
-                na = cmul(make_double2(na.x * invL, na.y * invL), cn);
-                nb = cmul(make_double2(nb.x * invL, nb.y * invL), cn);
-            }
-            if (ho[i].ncols > 0) {
-                double2 *e = reinterpret_cast<double2 *>(
-                    arena + ((int64_t)ho[i].y + (int64_t)rr * ho[i].x) * ew);
-                e[0] = make_double2(w * (sa.x - sb.x), w * (sa.y - sb.y));
-                e[1] = am > 0 ? make_double2(w * (na.x - nb.x), w * (na.y - nb.y))
-                              : make_double2(0.0, 0.0);
-            }
-            if (he[i].ncols > 0) {
-                double2 *e = reinterpret_cast<double2 *>(
-                    arena + ((int64_t)he[i].y + (int64_t)rr * he[i].x) * ew);
-                e[0] = make_double2(w * (sa.x + sb.x), w * (sa.y + sb.y));
-                e[1] = am > 0 ? make_double2(w * (na.x + nb.x), w * (na.y + nb.y))
-                              : make_double2(0.0, 0.0);
-            }
-        }
-    }
-    __syncthreads();
-    }
-}
-
 // ---- row-pair kernels on a 2-CTA cluster (rows that fit a CTA's half SM)
 //
-// The pair kernels above hold both rows n+r / n-1-r in one CTA (128 KB of
-// shared memory at N=1024 plus the twiddles), so one CTA of 8 warps runs
-// per SM and its load, transform and store phases serialize (ncu: 12%
-// occupancy, long-scoreboard stalls).  Here the pair is a thread-block
+// Round 1 held both rows n+r / n-1-r in one CTA (128 KB of shared memory
+// at N=1024 plus the twiddles): one CTA of 8 warps per SM, load, transform
+// and store phases serialized (ncu: 12% occupancy).  Here the pair is a
+// thread-block
 // cluster of two CTAs, one row each (rank 0: row n+r, rank 1: row n-1-r),
 // 64 KB of shared memory and <= 128 registers per thread, so two clusters'
 // CTAs share an SM and one CTA's DRAM phase overlaps another's transform.
@@ -1280,17 +996,6 @@ int dft_gen_bytes(const std::vector<int> &rad) {
         if (p > 13) return kGenBytes;
     return 0;
 }
-// shared-memory layouts (bytes); gen = the generic-radix staging at the tail
-bool dft_w_smem(int64_t L, int gen) { return 3 * L * 16 + gen <= 227 * 1024; }
-int dft_pair_smem(int64_t L, int gen) { return dft_smem_bytes(L, dft_w_smem(L, gen) ? 3 : 2) + gen; }
-// analysis kernel: + node-half bases (int32 per half) when they fit too
-bool dft_y_smem(int64_t L, int64_t nh, int gen) {
-    return dft_w_smem(L, gen) && 3 * L * 16 + 4 * nh + gen <= 227 * 1024;
-}
-int dft_anal_smem(int64_t L, int64_t nh, int gen) {
-    return dft_pair_smem(L, gen) + (dft_y_smem(L, nh, gen) ? (int)(4 * nh) : 0);
-}
-
 }  // namespace
 
 // Tables of the length-L DFT stage (built once per length, on the plan's
@@ -1431,7 +1136,6 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     pl->dft_gen = dft_gen_bytes(rad);
     const int gen = pl->dft_gen;
     // global scratch rows for rows longer than half an SM's shared memory
-    // (the legacy one-CTA pair kernels use it when two rows exceed a CTA's)
     if (Lb * 16 + gen > kPairSmemMax) {
         const int64_t rows = 2 * (int64_t)pl->sm_count * 4;
         BF_CUDA(cudaMalloc(&pl->dft_scratch, 16 * Lb * rows));
@@ -1441,27 +1145,14 @@ int bf_dft_prepare(bfsht_plan *pl, int64_t L) {
     return 0;
 }
 
-static int dft_grid_limit(const bfsht_plan *pl) {
-    return pl->dft_scratch ? (int)(pl->dft_scratch_rows / 2) : (1 << 30);
-}
-
 // DFT-stage kernel choice.  A row in half an SM's shared memory: rows in
-// shared memory, two CTAs per SM (synthesis one row per CTA, analysis a
-// 2-CTA cluster per row pair).  Longer rows: the same kernels over global
-// (L2-resident) scratch rows, persistent.  BFSHT_DFT_LEGACY=1 selects the
-// one-CTA row-pair kernels (both rows in one CTA) for A/B measurements;
-// BFSHT_DFT_SYNTH=row the one-row synthesis for short rows too (measured
-// N=1024: cluster 0.204 ms, row 0.245 ms, legacy 0.209 ms).
-static bool legacy_path() {
-    static const bool v = std::getenv("BFSHT_DFT_LEGACY") != nullptr;
-    return v;
-}
+// shared memory, two CTAs per SM, a 2-CTA cluster per row pair (measured
+// at N=1024 against the round-1 kernels that held both rows in one CTA:
+// synthesis 0.204 vs 0.209 ms, and a one-row-per-CTA synthesis without the
+// cluster 0.245 ms).  Longer rows: global (L2-resident) scratch rows,
+// persistent grids (synthesis one row per CTA, analysis the cluster pair).
 static bool pair_path(const bfsht_plan *pl) {
-    return !legacy_path() && pl->dft_Lb * 16 + pl->dft_gen <= kPairSmemMax;
-}
-static bool cluster_synth() {
-    static const char *v = std::getenv("BFSHT_DFT_SYNTH");
-    return !(v && std::strcmp(v, "row") == 0);
+    return pl->dft_Lb * 16 + pl->dft_gen <= kPairSmemMax;
 }
 static int scratch_grid(const bfsht_plan *pl, int r_count) {
     const int64_t g = std::min<int64_t>(2LL * r_count, pl->dft_scratch_rows) & ~1LL;
@@ -1481,37 +1172,21 @@ static int launch_synth(bfsht_plan *pl, const bf_half *halves, const double *are
     const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
     const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
     double2 *g = reinterpret_cast<double2 *>(grid);
-    if (pair_path(pl) && cluster_synth()) {
+    if (pair_path(pl)) {
         const int smem = (int)(pl->dft_Lb * 16) + pl->dft_gen;
         auto kern = pl->dft_gen ? sht_synth_pair_kernel<true> : sht_synth_pair_kernel<false>;
         int rc = bf_ensure_smem((const void *)kern, smem);
         if (rc) return rc;
         kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw,
                                                      pl->dft_perm, W, g, yr, ystride, ew, chirp, H);
-    } else if (!legacy_path()) {
-        const bool sm = pair_path(pl);
-        const int smem = sm ? (int)(pl->dft_Lb * 16) + pl->dft_gen : pl->dft_gen;
-        auto kern = sm ? (pl->dft_gen ? sht_synth_row_kernel<true, true>
-                                      : sht_synth_row_kernel<true, false>)
-                       : (pl->dft_gen ? sht_synth_row_kernel<false, true>
-                                      : sht_synth_row_kernel<false, false>);
-        const int grid = sm ? 2 * r_count : scratch_grid(pl, r_count);
-        int rc = bf_ensure_smem((const void *)kern, smem);
-        if (rc) return rc;
-        kern<<<grid, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw, pl->dft_perm, W, g,
-                                              yr, ystride, ew, chirp, H,
-                                              reinterpret_cast<double2 *>(pl->dft_scratch));
     } else {
-        const bool sm = dft_pair_smem(pl->dft_Lb, pl->dft_gen) <= 227 * 1024;
-        const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-        const int smem = sm ? dft_pair_smem(pl->dft_Lb, pl->dft_gen) : pl->dft_gen;
-        auto kern = sm ? sht_synth_kernel<true> : sht_synth_kernel<false>;
-        int rc = bf_ensure_smem((const void *)kern, smem);
+        auto kern = pl->dft_gen ? sht_synth_row_kernel<false, true>
+                                : sht_synth_row_kernel<false, false>;
+        int rc = bf_ensure_smem((const void *)kern, pl->dft_gen);
         if (rc) return rc;
-        kern<<<nblk, kDftThreads, smem, st>>>(
-            d, n, halves, arena, r_begin, r_count, tw, pl->dft_perm, W, g, sm,
-            reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen), yr,
-            ystride, ew, chirp, H);
+        kern<<<scratch_grid(pl, r_count), kDftThreads, pl->dft_gen, st>>>(
+            d, n, halves, arena, r_count, tw, pl->dft_perm, W, g, yr, ystride, ew, chirp, H,
+            reinterpret_cast<double2 *>(pl->dft_scratch));
     }
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
@@ -1530,35 +1205,18 @@ static int launch_anal(bfsht_plan *pl, const bf_half *halves, double *arena, int
     const double2 *chirp = reinterpret_cast<const double2 *>(pl->dft_chirp);
     const double2 *H = reinterpret_cast<const double2 *>(pl->dft_hhat);
     const double2 *g = reinterpret_cast<const double2 *>(grid);
-    if (!legacy_path()) {
-        const bool sm = pair_path(pl);
-        const int smem = sm ? (int)(pl->dft_Lb * 16) + pl->dft_gen : pl->dft_gen;
-        auto kern = sm ? (pl->dft_gen ? sht_anal_pair_kernel<true, true>
-                                      : sht_anal_pair_kernel<true, false>)
-                       : (pl->dft_gen ? sht_anal_pair_kernel<false, true>
-                                      : sht_anal_pair_kernel<false, false>);
-        const int grid = sm ? 2 * r_count : scratch_grid(pl, r_count);
-        int rc = bf_ensure_smem((const void *)kern, smem);
-        if (rc) return rc;
-        kern<<<grid, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g, weights,
-                                              r_begin, r_count, node_y, ew, chirp, H,
-                                              reinterpret_cast<double2 *>(pl->dft_scratch));
-    } else {
-        const bool sm = dft_pair_smem(pl->dft_Lb, pl->dft_gen) <= 227 * 1024;
-        const int nblk = std::min(std::min(r_count, pl->sm_count), dft_grid_limit(pl));
-        const int64_t nh = 2 * (int64_t)pl->norders;
-        const bool ysm = node_y && sm && dft_y_smem(pl->dft_Lb, nh, pl->dft_gen);
-        const int smem = sm ? (ysm ? dft_anal_smem(pl->dft_Lb, nh, pl->dft_gen)
-                                   : dft_pair_smem(pl->dft_Lb, pl->dft_gen))
-                            : pl->dft_gen;
-        auto kern = sm ? sht_anal_kernel<true> : sht_anal_kernel<false>;
-        int rc = bf_ensure_smem((const void *)kern, smem);
-        if (rc) return rc;
-        kern<<<nblk, kDftThreads, smem, st>>>(
-            d, n, halves, arena, tw, pl->dft_perm, W, g, weights, r_begin, r_count, sm,
-            reinterpret_cast<double2 *>(pl->dft_scratch), dft_w_smem(pl->dft_Lb, pl->dft_gen),
-            ysm ? node_y : nullptr, (int)nh, ew, chirp, H);
-    }
+    const bool sm = pair_path(pl);
+    const int smem = sm ? (int)(pl->dft_Lb * 16) + pl->dft_gen : pl->dft_gen;
+    auto kern = sm ? (pl->dft_gen ? sht_anal_pair_kernel<true, true>
+                                  : sht_anal_pair_kernel<true, false>)
+                   : (pl->dft_gen ? sht_anal_pair_kernel<false, true>
+                                  : sht_anal_pair_kernel<false, false>);
+    const int nblk = sm ? 2 * r_count : scratch_grid(pl, r_count);
+    int rc = bf_ensure_smem((const void *)kern, smem);
+    if (rc) return rc;
+    kern<<<nblk, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g, weights,
+                                          r_begin, r_count, node_y, ew, chirp, H,
+                                          reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
     pl->launches += 1;
     return 0;

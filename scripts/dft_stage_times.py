@@ -66,9 +66,7 @@ for n in [int(v) for v in args.n.split(",")]:
         ms = timed(fn, reps)
         gbs = nbytes / (ms * 1e-3) / 1e9
         print(json.dumps({"n": n, "L": L, "kernel": name, "ms": ms, "alg_bytes": nbytes,
-                          "GBps": gbs, "frac_of_peak": gbs / pk,
-                          "path": "legacy" if os.environ.get("BFSHT_DFT_LEGACY") else "cluster"}),
-              flush=True)
+                          "GBps": gbs, "frac_of_peak": gbs / pk}), flush=True)
     run.close()
     del grid, run
     torch.cuda.empty_cache()

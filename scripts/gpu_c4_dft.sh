@@ -2,16 +2,12 @@
 mkdir -p gpurun_out
 python -m paper_2004_11346_b200.build > gpurun_out/build.log 2>&1 || tail -5 gpurun_out/build.log
 timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_fields.py tests/test_gpu_sht.py tests/test_gpu_c2_parity.py tests/test_gpu_dft_big.py tests/test_gpu_pipeline.py tests/test_gpu_sharded.py tests/test_gpu_ooc.py 2>&1 | tail -3
-for v in cluster row legacy; do
-  unset BFSHT_DFT_LEGACY BFSHT_DFT_SYNTH
-  [ $v = legacy ] && export BFSHT_DFT_LEGACY=1
-  [ $v = row ] && export BFSHT_DFT_SYNTH=row
+for v in current; do
   echo "== $v"; timeout 600 python scripts/dft_stage_times.py --n ${DFT_NS:-1024,2048,4096} 2>&1 | grep '"kernel"' | python -c "
 import sys,json
 for l in sys.stdin:
     d=json.loads(l); print(d['n'], d['kernel'], round(d['ms'],4), round(d['frac_of_peak'],3))"
 done
-unset BFSHT_DFT_LEGACY BFSHT_DFT_SYNTH
 for v in group wide16; do
   unset BFSHT_FIELDS_WIDE16; [ $v = wide16 ] && export BFSHT_FIELDS_WIDE16=1
   timeout 900 python bench.py --workload c4 --steps 5 --warmup 3 > gpurun_out/bench_c4_$v.json 2> gpurun_out/bench_c4_$v.err
