@@ -129,7 +129,11 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out);
  * order), dev[6] = vector arena (info[5] x 4 doubles), dev[7] = recurrence
  * coefficients, dev[8] = x_pos (both only read by regenerated tiles, may
  * be NULL when info[18] == 0), dev[9..11] reserved (NULL); host[5..7] =
- * host copies of halves and the two stage-bound arrays. */
+ * host copies of halves and the two stage-bound arrays; host[1] and
+ * host[4] = host copies of ops and tasks (optional, both or neither: with
+ * them the butterfly-chain stages get their bundle schedule and run on the
+ * chain kernel; without them every stage runs on the stage kernel — same
+ * results, bit for bit). */
 int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8],
                     void *const dev[12], bfsht_plan **out);
 void bfsht_plan_free(bfsht_plan *pl);

@@ -112,6 +112,10 @@ class DevicePlan:
             self._si = np.ascontiguousarray(pk.stages_inv)
             info = (ctypes.c_int64 * INFO_LEN)(*[int(v) for v in pk.info])
             host = (ctypes.c_void_p * 8)()
+            if pk.ops.size and pk.tasks.size:
+                # host copies of ops / tasks: the chain-stage schedule
+                host[1] = pk.ops.ctypes.data
+                host[4] = pk.tasks.ctypes.data
             host[5] = self._host_halves.ctypes.data
             host[6] = self._sf.ctypes.data
             host[7] = self._si.ctypes.data

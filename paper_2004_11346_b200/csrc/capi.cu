@@ -43,7 +43,7 @@ int bf_dft_rows(bfsht_plan *pl, int64_t L, int64_t rows, int dir, const double *
 namespace {
 
 int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
-                const int64_t *si) {
+                const int64_t *si, const bf_op *host_ops, const bf_task *host_tasks) {
     const int64_t nh = pl->info[6];
     pl->stages[0].assign(sf, sf + pl->info[7] + 1);
     pl->stages[1].assign(si, si + pl->info[8] + 1);
@@ -94,7 +94,7 @@ int finish_plan(bfsht_plan *pl, const bf_half *host_halves, const int64_t *sf,
     BF_CUDA(cudaGetDevice(&dev));
     pl->device = dev;
     BF_CUDA(cudaDeviceGetAttribute(&pl->sm_count, cudaDevAttrMultiProcessorCount, dev));
-    return 0;
+    return bf_chain_build(pl, host_ops, host_tasks);
 }
 
 }  // namespace
@@ -158,7 +158,7 @@ int bfsht_plan_upload(const bfsht_packed *p, bfsht_plan **out) {
     pl->xpos = (const double *)dev[7];
     pl->arena = (double *)arena;
     int rc = finish_plan(pl, (const bf_half *)arr[5], (const int64_t *)arr[6],
-                         (const int64_t *)arr[7]);
+                         (const int64_t *)arr[7], (const bf_op *)arr[1], (const bf_task *)arr[4]);
     if (rc) {
         bfsht_plan_free(pl);
         return rc;
@@ -190,7 +190,8 @@ int bfsht_plan_wrap(const int64_t info[BFSHT_INFO_LEN], const void *const host[8
         return -1;
     }
     int rc = finish_plan(pl, (const bf_half *)host[5], (const int64_t *)host[6],
-                         (const int64_t *)host[7]);
+                         (const int64_t *)host[7], (const bf_op *)host[1],
+                         (const bf_task *)host[4]);
     if (rc) {
         bfsht_plan_free(pl);
         return rc;
@@ -237,8 +238,7 @@ int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
         g_err = "stage out of range";
         return -1;
     }
-    return bf_run_stage(pl, b[stage], b[stage + 1], pl->counters + stage, (cudaStream_t)stream,
-                        0);
+    return bf_run_stage(pl, dir, stage, (cudaStream_t)stream);
 }
 
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,

@@ -31,7 +31,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <queue>
 
 #include "engine.cuh"
 #include "recur.h"
@@ -780,6 +783,301 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
     }
 }
 
+// ------------------------------------------------------------ chain engine
+// The butterfly-chain and low-rank-core stages are made of small tasks (3-9
+// ops, tiles of 2-6 KB, 32-byte gathers, 20-35% index adds).  On
+// alt_stage_kernel they ran at under half of the HBM roofline, and ncu put
+// that on instruction issue, not on memory: ~600 warp instructions per op
+// (task claims, cursor and record bookkeeping ~60% of them) with warps
+// stalled on fixed-latency dependencies and on the record / claim loads.
+// alt_chain_kernel runs the same ops, in the same per-task order (results
+// are bitwise those of alt_stage_kernel), from a schedule built once per
+// plan (bf_chain_build):
+//  * one 32-byte record per op carrying everything the warp needs (tile,
+//    input, lane map, shape, the task's output range on its last op), read
+//    as two 16-byte loads two ops ahead — no task records, no cursor;
+//  * tasks pre-grouped into cost-balanced bundles (LPT) that a warp claims
+//    with one atomic per bundle instead of one per task;
+//  * an index add that follows a tile op is folded into that op's record:
+//    its gathered entries land in the free tail of the tile slot and are
+//    added right after the tile product, so it costs no ring slot, no
+//    barrier wait and no op of its own.
+struct ChainArgs {
+    const double *tiles;
+    const int4 *rec;         // bf_crec records as two int4 each
+    const int32_t *bund;     // the stage's bundle bounds (nb + 1 record indices)
+    const int32_t *idx;
+    const int8_t *maps;
+    double *arena;
+    int nb;
+    int *counter;
+};
+
+struct alignas(128) ChainRing {
+    double tile[kStages][kTileDoubles];
+    double vec[kStages][BF_T * BF_NRHS];
+    int8_t map[kStages][BF_SLOTS];
+    double zero[16];
+    int4 meta[kStages][2];
+    unsigned long long full[kStages];
+};
+static_assert(sizeof(ChainRing) * kWarps <= 227 * 1024, "chain ring exceeds shared memory");
+static_assert(sizeof(bf_crec) == 32, "chain record is two int4");
+static_assert(BF_FOLD_AT + BF_T * BF_NRHS <= kTileDoubles, "folded add past the tile slot");
+
+// a: tile, in, aux, kind | R << 8 | C << 16 | off << 24
+// b: flags | addR << 8 | addoff << 16, add_in, out, nout
+struct CRec {
+    int4 a, b;
+};
+
+__device__ __forceinline__ CRec load_crec(const ChainArgs &a, int i) {
+    CRec r;
+    const int4 *p = a.rec + 2 * (int64_t)i;
+    r.a = __ldg(p);
+    r.b = __ldg(p + 1);
+    return r;
+}
+
+struct CStream {
+    int pos, end;       // records of the current bundle
+    int npos, nend;     // the next bundle (claimed, bounds loaded)
+    int raw;            // lane 0: id of the bundle after next
+};
+
+__device__ __forceinline__ int chain_claim(const ChainArgs &a, int lane) {
+    return lane == 0 ? atomicAdd(a.counter, 1) : 0;
+}
+
+// index of the next record of this warp's stream, -1 at the end
+__device__ __forceinline__ int chain_next(const ChainArgs &a, CStream &c, int lane) {
+    if (c.pos >= c.end) {
+        if (c.npos >= c.nend) return -1;
+        c.pos = c.npos;
+        c.end = c.nend;
+        const int nb = bcast(c.raw);
+        if (nb < a.nb) {
+            c.npos = __ldg(a.bund + nb);
+            c.nend = __ldg(a.bund + nb + 1);
+            c.raw = chain_claim(a, lane);
+        } else {
+            c.npos = c.nend = 0;
+        }
+    }
+    return c.pos++;
+}
+
+// gather sources of this lane for record r (-1: none), loaded one op early
+__device__ __forceinline__ int chain_gsrc(const ChainArgs &a, const CRec &r, int lane) {
+    const uint32_t w = (uint32_t)r.a.w;
+    if (!(r.b.x & BF_OPF_GATHER)) return -1;
+    const int kind = w & 0xff, R = (w >> 8) & 0xff, C = (w >> 16) & 0xff;
+    const int nvec = kind == BF_OP_TILE_N ? C : R;
+    return lane < nvec ? __ldg(a.idx + r.a.y + lane) : -1;
+}
+
+__device__ __forceinline__ int chain_gadd(const ChainArgs &a, const CRec &r, int lane) {
+    if (!(r.b.x & BF_CF_ADD)) return -1;
+    const int addR = ((uint32_t)r.b.x >> 8) & 0xff;
+    return lane < addR ? __ldg(a.idx + r.b.y + lane) : -1;
+}
+
+__device__ __forceinline__ void chain_issue(const ChainArgs &a, ChainRing &ring, int s,
+                                            const CRec &r, int gsrc, int gadd, int lane) {
+    const uint32_t w = (uint32_t)r.a.w, f = (uint32_t)r.b.x;
+    const int kind = w & 0xff, R = (w >> 8) & 0xff, C = (w >> 16) & 0xff;
+    const bool gather = (f & BF_OPF_GATHER) != 0;
+    if (lane == 0) {
+        ring.meta[s][0] = r.a;
+        ring.meta[s][1] = r.b;
+    }
+    const int nvec = kind == BF_OP_TILE_N ? C : R;
+    const uint32_t tb = kind == BF_OP_ADD ? 0u : (uint32_t)(((R + 3) >> 2) * ((C + 3) >> 2)) * 128u;
+    if (gather) {
+        double *d = &ring.vec[s][lane * BF_NRHS];
+        if (gsrc >= 0) {
+            const double *gp = a.arena + (int64_t)gsrc * BF_NRHS;
+            cp_async16(d, gp);
+            cp_async16(d + 2, gp + 2);
+        } else if (kind == BF_OP_ADD) {
+            // lanes without a source add zeros
+            *reinterpret_cast<double2 *>(d) = make_double2(0.0, 0.0);
+            *reinterpret_cast<double2 *>(d + 2) = make_double2(0.0, 0.0);
+        }
+    }
+    if (f & BF_CF_ADD) {
+        double *d = ring.tile[s] + BF_FOLD_AT + lane * BF_NRHS;
+        if (gadd >= 0) {
+            const double *gp = a.arena + (int64_t)gadd * BF_NRHS;
+            cp_async16(d, gp);
+            cp_async16(d + 2, gp + 2);
+        } else {
+            *reinterpret_cast<double2 *>(d) = make_double2(0.0, 0.0);
+            *reinterpret_cast<double2 *>(d + 2) = make_double2(0.0, 0.0);
+        }
+    }
+    cp_async_arrive(&ring.full[s]);
+    if (lane == 0) {
+        const bool lanemap = (f & BF_OPF_LANEMAP) != 0;
+        const uint32_t vb = gather ? 0u : (uint32_t)nvec * (BF_NRHS * 8u);
+        fence_proxy_async();
+        mbar_arrive_tx(&ring.full[s], tb + vb + (lanemap ? (uint32_t)BF_SLOTS : 0u));
+        if (tb) bulk_g2s(ring.tile[s], a.tiles + (int64_t)(uint32_t)r.a.x * 16, tb, &ring.full[s]);
+        if (vb) bulk_g2s(ring.vec[s], a.arena + (int64_t)r.a.y * BF_NRHS, vb, &ring.full[s]);
+        if (lanemap)
+            bulk_g2s(ring.map[s], a.maps + (int64_t)r.a.z * BF_SLOTS, BF_SLOTS, &ring.full[s]);
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1) alt_chain_kernel(ChainArgs a) {
+    constexpr int NR = BF_NRHS, QACT = Width<NR>::QACT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    ChainRing &ring = reinterpret_cast<ChainRing *>(smem_raw)[warp];
+    {
+        double2 *z = reinterpret_cast<double2 *>(&ring);
+        const int n2 = (int)(offsetof(ChainRing, meta) / sizeof(double2));
+        for (int i = lane; i < n2; i += 32) z[i] = make_double2(0.0, 0.0);
+    }
+    if (lane == 0) {
+        for (int s = 0; s < kStages; ++s) mbar_init(&ring.full[s], 33);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int g = lane >> 2, q = lane & 3;
+
+    CStream cs;
+    cs.pos = cs.end = cs.npos = cs.nend = 0;
+    cs.raw = 0;
+    {
+        const int first = bcast(chain_claim(a, lane));
+        if (first < a.nb) {
+            cs.npos = __ldg(a.bund + first);
+            cs.nend = __ldg(a.bund + first + 1);
+            cs.raw = chain_claim(a, lane);
+        }
+    }
+    CRec r0, r1;
+    r0.a = r0.b = r1.a = r1.b = make_int4(0, 0, 0, 0);
+    int i0 = chain_next(a, cs, lane);
+    if (i0 >= 0) r0 = load_crec(a, i0);
+    int g0 = i0 >= 0 ? chain_gsrc(a, r0, lane) : -1;
+    int ga0 = i0 >= 0 ? chain_gadd(a, r0, lane) : -1;
+    int i1 = i0 >= 0 ? chain_next(a, cs, lane) : -1;
+    if (i1 >= 0) r1 = load_crec(a, i1);
+    uint32_t seq_issue = 0, seq_use = 0;
+    auto issue_next = [&]() {
+        chain_issue(a, ring, seq_issue % kStages, r0, g0, ga0, lane);
+        ++seq_issue;
+        r0 = r1;
+        i0 = i1;
+        if (i0 >= 0) {
+            g0 = chain_gsrc(a, r0, lane);
+            ga0 = chain_gadd(a, r0, lane);
+            i1 = chain_next(a, cs, lane);
+            if (i1 >= 0) r1 = load_crec(a, i1);
+        }
+    };
+    while (i0 >= 0 && seq_issue - seq_use < kStages) issue_next();
+
+    double acc[1][8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[0][j][0] = acc[0][j][1] = 0.0;
+
+    while (seq_use < seq_issue) {
+        const int s = seq_use % kStages;
+        mbar_wait(&ring.full[s], (seq_use / kStages) & 1u);
+        ++seq_use;
+        const int4 ma = ring.meta[s][0], mb = ring.meta[s][1];
+        const uint32_t w = (uint32_t)ma.w, f = (uint32_t)mb.x;
+        bf_op op;
+        op.kind = (uint8_t)(w & 0xff);
+        op.R = (uint8_t)((w >> 8) & 0xff);
+        op.C = (uint8_t)((w >> 16) & 0xff);
+        op.off = (uint8_t)(w >> 24);
+        const double *V = ring.vec[s];
+        if (op.kind == BF_OP_ADD) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int jj = 8 * j + g - op.off;
+                if (q < QACT && jj >= 0 && jj < op.R) {
+                    const double2 v = *reinterpret_cast<const double2 *>(V + jj * NR + 2 * q);
+                    acc[0][j][0] += v.x;
+                    acc[0][j][1] += v.y;
+                }
+            }
+        } else {
+            double e[1][4][2];
+            tile_product<NR>(op, ring.tile[s], V, ring.zero, lane, e);
+            const bool lanemap = (f & BF_OPF_LANEMAP) != 0;
+            if (!lanemap && (op.off & 7) == 0) {
+                switch (op.off >> 3) {
+                    case 0: place_tiles<1, 0>(acc, e); break;
+                    case 1: place_tiles<1, 1>(acc, e); break;
+                    case 2: place_tiles<1, 2>(acc, e); break;
+                    case 3: place_tiles<1, 3>(acc, e); break;
+                    case 4: place_tiles<1, 4>(acc, e); break;
+                    case 5: place_tiles<1, 5>(acc, e); break;
+                    case 6: place_tiles<1, 6>(acc, e); break;
+                    default: place_tiles<1, 7>(acc, e); break;
+                }
+            } else {
+                // general placement through the slot's (now dead) input vector
+                double *S = ring.vec[s];
+                __syncwarp();
+                const int width = (op.kind == BF_OP_TILE_N) ? op.R : op.C;
+                const int MT = (width + 7) >> 3;
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+                    if (mt < MT && q < QACT)
+                        *reinterpret_cast<double2 *>(S + (8 * mt + g) * NR + 2 * q) =
+                            make_double2(e[0][mt][0], e[0][mt][1]);
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int sl = 8 * j + g;
+                    const int src = lanemap ? (int)ring.map[s][sl] : sl - op.off;
+                    if (q < QACT && src >= 0 && src < width) {
+                        const double2 v = *reinterpret_cast<const double2 *>(S + src * NR + 2 * q);
+                        acc[0][j][0] += v.x;
+                        acc[0][j][1] += v.y;
+                    }
+                }
+                __syncwarp();
+            }
+            if (f & BF_CF_ADD) {
+                // folded index add: entry jj adds into slot addoff + jj
+                const int addR = (f >> 8) & 0xff, addoff = (f >> 16) & 0xff;
+                const double *A = ring.tile[s] + BF_FOLD_AT;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int jj = 8 * j + g - addoff;
+                    if (q < QACT && jj >= 0 && jj < addR) {
+                        const double2 v = *reinterpret_cast<const double2 *>(A + jj * NR + 2 * q);
+                        acc[0][j][0] += v.x;
+                        acc[0][j][1] += v.y;
+                    }
+                }
+            }
+        }
+        if (f & BF_CF_LAST) {
+            const int nout = mb.w & 0xff;
+            const int stride = (mb.w >> 8) ? (mb.w >> 8) : 1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int sl = 8 * j + g;
+                if (q < QACT && sl < nout) {
+                    double *o = a.arena + ((int64_t)mb.z + (int64_t)sl * stride) * NR + 2 * q;
+                    *reinterpret_cast<double2 *>(o) = make_double2(acc[0][j][0], acc[0][j][1]);
+                }
+                acc[0][j][0] = acc[0][j][1] = 0.0;
+            }
+        }
+        __syncwarp();
+        while (i0 >= 0 && seq_issue - seq_use < kStages) issue_next();
+    }
+}
+
 // ------------------------------------------------------------ group engine
 // Batched fields with many fields per payload pass (BASELINE config 4, the
 // "real dense contraction" of north_star (2)).  The warp engine above gives
@@ -1108,10 +1406,188 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
     return 0;
 }
 
-int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, cudaStream_t st,
-                 int max_ctas) {
-    if (t1 <= t0) return 0;
-    return launch_stage<BF_NRHS>(pl, t0, t1, counter, pl->arena, st, max_ctas, true);
+// ---------------------------------------------------------- chain schedule
+static int env_int(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// BFSHT_CHAIN: 0 = every stage on alt_stage_kernel; 1 (default) = stages
+// holding gather / lane-map ops (the butterfly chain; stage 0 also carries
+// the low-rank cores) on alt_chain_kernel; 2 = every stage without
+// regenerated tiles.  BFSHT_CHAIN_BUNDLES: bundles per warp (default 6).
+// BFSHT_CHAIN_CFIX: fixed cost of an op in bytes-equivalents for the bundle
+// balance (default 3072).
+int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
+    const int mode = env_int("BFSHT_CHAIN", 1);
+    if (!ops || !tasks || mode <= 0) return 0;
+    const int per_warp = std::max(1, env_int("BFSHT_CHAIN_BUNDLES", 6));
+    const double cfix = (double)std::max(0, env_int("BFSHT_CHAIN_CFIX", 3072));
+    const int64_t W = (int64_t)pl->sm_count * kWarps;
+    std::vector<bf_crec> recs;
+    std::vector<int32_t> bund;
+    struct TaskSpan {
+        int64_t r0;
+        int n;
+        double cost;
+    };
+    std::vector<bf_crec> trec;
+    std::vector<TaskSpan> spans;
+    for (int d = 0; d < 2; ++d) {
+        const std::vector<int64_t> &b = pl->stages[d];
+        const int nst = (int)b.size() - 1;
+        pl->chain[d].assign(nst > 0 ? nst : 0, bfsht_plan::ChainStage());
+        for (int s = 0; s < nst; ++s) {
+            const int64_t t0 = b[s], t1 = b[s + 1];
+            if (t1 <= t0) continue;
+            bool regen = false, small = false;
+            for (int64_t t = t0; t < t1 && !regen; ++t)
+                for (int i = 0; i < tasks[t].op_count; ++i) {
+                    const uint8_t f = ops[tasks[t].op_begin + i].flags;
+                    if (f & BF_OPF_REGEN) regen = true;
+                    if (f & (BF_OPF_GATHER | BF_OPF_LANEMAP)) small = true;
+                }
+            if (regen || (mode == 1 && !small)) continue;
+            trec.clear();
+            spans.clear();
+            for (int64_t t = t0; t < t1; ++t) {
+                const bf_task &tk = tasks[t];
+                TaskSpan sp;
+                sp.r0 = (int64_t)trec.size();
+                sp.cost = 0.0;
+                bool have_prev = false;
+                for (int i = 0; i < tk.op_count; ++i) {
+                    const bf_op &o = ops[tk.op_begin + i];
+                    if (o.tile % 16 != 0 || o.tile / 16 > (int64_t)UINT32_MAX) {
+                        bfsht_set_error("tile offset not representable in a chain record");
+                        return -3;
+                    }
+                    if (o.kind == BF_OP_ADD && (o.flags & BF_OPF_GATHER) && have_prev) {
+                        bf_crec &pr = trec.back();
+                        if (pr.kind != BF_OP_ADD && !(pr.flags & BF_CF_ADD) &&
+                            bf_tile_doubles(pr.R, pr.C) <= BF_FOLD_AT && o.R <= BF_T) {
+                            pr.flags |= BF_CF_ADD;
+                            pr.addR = o.R;
+                            pr.addoff = o.off;
+                            pr.add_in = o.in;
+                            sp.cost += 32.0 * o.R;
+                            continue;
+                        }
+                    }
+                    bf_crec c;
+                    std::memset(&c, 0, sizeof(c));
+                    c.tile = (uint32_t)(o.tile / 16);
+                    c.in = o.in;
+                    c.aux = o.aux;
+                    c.kind = o.kind;
+                    c.R = o.R;
+                    c.C = o.C;
+                    c.off = o.off;
+                    c.flags = (uint8_t)(o.flags & (BF_OPF_GATHER | BF_OPF_LANEMAP));
+                    trec.push_back(c);
+                    have_prev = true;
+                    sp.cost += cfix + (o.kind == BF_OP_ADD
+                                           ? 32.0 * o.R
+                                           : 8.0 * (double)bf_tile_doubles(o.R, o.C) +
+                                                 32.0 * (o.kind == BF_OP_TILE_N ? o.C : o.R));
+                }
+                if ((int64_t)trec.size() == sp.r0) {
+                    bfsht_set_error("task without ops");
+                    return -3;
+                }
+                bf_crec &last = trec.back();
+                last.flags |= BF_CF_LAST;
+                last.out = tk.out;
+                last.nout = tk.nout;
+                sp.n = (int)((int64_t)trec.size() - sp.r0);
+                spans.push_back(sp);
+            }
+            // LPT: tasks by descending cost onto the least-loaded bundle
+            const int64_t ntasks = t1 - t0;
+            const int nb = (int)std::min<int64_t>(ntasks, W * per_warp);
+            std::vector<int32_t> order(ntasks);
+            for (int64_t i = 0; i < ntasks; ++i) order[i] = (int32_t)i;
+            std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+                return spans[x].cost > spans[y].cost;
+            });
+            std::vector<std::vector<int32_t>> members(nb);
+            std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>,
+                                std::greater<std::pair<double, int>>>
+                heap;
+            for (int i = 0; i < nb; ++i) heap.push({0.0, i});
+            for (int32_t t : order) {
+                auto top = heap.top();
+                heap.pop();
+                members[top.second].push_back(t);
+                heap.push({top.first + spans[t].cost, top.second});
+            }
+            pl->chain[d][s].b0 = (int64_t)bund.size();
+            pl->chain[d][s].nb = nb;
+            for (int i = 0; i < nb; ++i) {
+                bund.push_back((int32_t)recs.size());
+                for (int32_t t : members[i])
+                    recs.insert(recs.end(), trec.begin() + spans[t].r0,
+                                trec.begin() + spans[t].r0 + spans[t].n);
+                if ((int64_t)recs.size() > INT32_MAX) {
+                    bfsht_set_error("chain records exceed int32");
+                    return -3;
+                }
+            }
+            bund.push_back((int32_t)recs.size());
+        }
+    }
+    if (recs.empty()) {
+        for (int d = 0; d < 2; ++d)
+            for (auto &c : pl->chain[d]) c.nb = 0;
+        return 0;
+    }
+    BF_CUDA(cudaMalloc(&pl->chain_rec, recs.size() * sizeof(bf_crec)));
+    pl->owned.push_back(pl->chain_rec);
+    BF_CUDA(cudaMemcpy(pl->chain_rec, recs.data(), recs.size() * sizeof(bf_crec),
+                       cudaMemcpyHostToDevice));
+    void *bd = nullptr;
+    BF_CUDA(cudaMalloc(&bd, bund.size() * sizeof(int32_t)));
+    pl->owned.push_back(bd);
+    pl->chain_bund = (int32_t *)bd;
+    BF_CUDA(cudaMemcpy(bd, bund.data(), bund.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    return 0;
+}
+
+static int launch_chain(bfsht_plan *pl, int dir, int s, int *counter, cudaStream_t st,
+                        bool reset) {
+    const bfsht_plan::ChainStage &c = pl->chain[dir][s];
+    const size_t smem = sizeof(ChainRing) * kWarps;
+    int rc = bf_ensure_smem((const void *)alt_chain_kernel, (int)smem);
+    if (rc) return rc;
+    ChainArgs a;
+    a.tiles = pl->tiles;
+    a.rec = (const int4 *)pl->chain_rec;
+    a.bund = pl->chain_bund + c.b0;
+    a.idx = pl->idx;
+    a.maps = pl->maps;
+    a.arena = pl->arena;
+    a.nb = c.nb;
+    a.counter = counter;
+    if (reset) BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
+    const int64_t want = ((int64_t)c.nb + kWarps - 1) / kWarps;
+    const int grid = (int)(want < pl->sm_count ? want : pl->sm_count);
+    alt_chain_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+    BF_CUDA(cudaGetLastError());
+    pl->launches += 1;
+    return 0;
+}
+
+static bool is_chain_stage(const bfsht_plan *pl, int dir, int s) {
+    return s < (int)pl->chain[dir].size() && pl->chain[dir][s].nb > 0;
+}
+
+int bf_run_stage(bfsht_plan *pl, int dir, int stage, cudaStream_t st) {
+    const std::vector<int64_t> &b = pl->stages[dir];
+    if (b[stage + 1] <= b[stage]) return 0;
+    if (is_chain_stage(pl, dir, stage))
+        return launch_chain(pl, dir, stage, pl->counters + stage, st, true);
+    return launch_stage<BF_NRHS>(pl, b[stage], b[stage + 1], pl->counters + stage, pl->arena, st,
+                                 0, true);
 }
 
 // All stages of one direction over a wide (16 RHS per entry) arena.
@@ -1142,8 +1618,10 @@ int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t st) {
     BF_CUDA(cudaMemsetAsync(pl->counters, 0, sizeof(int) * nst, st));
     for (int s = 0; s < nst; ++s) {
         if (b[s + 1] <= b[s]) continue;
-        int rc = launch_stage<BF_NRHS>(pl, b[s], b[s + 1], pl->counters + s, pl->arena, st, 0,
-                                       false);
+        int rc = is_chain_stage(pl, dir, s)
+                     ? launch_chain(pl, dir, s, pl->counters + s, st, false)
+                     : launch_stage<BF_NRHS>(pl, b[s], b[s + 1], pl->counters + s, pl->arena, st,
+                                             0, false);
         if (rc) return rc;
     }
     return 0;

@@ -52,6 +52,17 @@ struct bfsht_plan {
     int64_t launches = 0;
     int sm_count = 148;
     int device = 0;                   // CUDA device the plan lives on
+    // chain schedule (engine.cu, bf_chain_build): the stages made of small
+    // butterfly / low-rank-core tasks re-encoded as 32-byte records in
+    // cost-balanced bundles for alt_chain_kernel; nb == 0: the stage runs
+    // on alt_stage_kernel
+    struct ChainStage {
+        int64_t b0 = 0;               // first entry of the stage in chain_bund
+        int nb = 0;                   // bundles
+    };
+    std::vector<ChainStage> chain[2];
+    void *chain_rec = nullptr;        // device: bf_crec records, bundle after bundle
+    int32_t *chain_bund = nullptr;    // device: bundle bounds (record indices)
 };
 
 void bfsht_set_error(const std::string &msg);
@@ -90,8 +101,11 @@ struct DeviceGuard {
     } while (0)
 
 // engine.cu
-int bf_run_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter,
-                 cudaStream_t s, int max_ctas);
+int bf_run_stage(bfsht_plan *pl, int dir, int stage, cudaStream_t s);
+// Build the chain schedule from host copies of the plan's ops and tasks
+// (called once when the plan is created; without it every stage runs on
+// alt_stage_kernel).
+int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks);
 int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t s);
 int bf_alt_apply_wide(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);
 int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t s);

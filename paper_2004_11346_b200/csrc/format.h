@@ -90,6 +90,30 @@ typedef struct {
     int32_t nout;        /* entries written (<= 32) */
 } bf_task;               /* 16 bytes */
 
+/* Chain record: one op of a chain stage (small butterfly gather / scatter
+ * and low-rank-core tasks), re-encoded at plan-upload time from bf_op /
+ * bf_task for alt_chain_kernel (engine.cu).  Records of a task are
+ * consecutive; tasks are grouped in cost-balanced bundles that warps
+ * claim.  An index add that directly follows a tile op of its task rides
+ * on that op's record ("folded": BF_CF_ADD, add_in / addR / addoff), when
+ * the tile leaves the last BF_T entries of its ring slot free. */
+enum bf_crec_flags {
+    BF_CF_LAST = 8,      /* last op of its task: store the outputs */
+    BF_CF_ADD = 16       /* folded index add (gathered through idx[add_in + j]) */
+};
+#define BF_FOLD_AT 896   /* doubles: where the folded add's entries land in the tile slot */
+
+typedef struct {
+    uint32_t tile;       /* tile offset in 16-double (128-byte) units */
+    int32_t in;          /* as bf_op.in */
+    int32_t aux;         /* lane-map index */
+    uint8_t kind, R, C, off;
+    uint8_t flags, addR, addoff, pad;
+    int32_t add_in;      /* idx offset of the folded add's sources */
+    int32_t out;         /* task: first arena entry written */
+    int32_t nout;        /* task: entries written | stride << 8 */
+} bf_crec;               /* 32 bytes */
+
 /* per (order, parity) half: where its vectors live */
 typedef struct {
     int32_t x;           /* coefficient half: ncols entries (fwd in, inv out) */

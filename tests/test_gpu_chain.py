@@ -1,0 +1,77 @@
+"""GPU: the chain kernel (alt_chain_kernel: bundle schedule, 32-byte records,
+folded index adds) runs the butterfly-chain stages bitwise like the stage
+kernel, and both match the oracle.  BFSHT_CHAIN is read when a device plan
+is created: 0 = every stage on alt_stage_kernel, 1 = default (stages with
+gather / lane-map ops on the chain kernel), 2 = every stage."""
+import numpy as np
+import pytest
+
+from paper_2004_11346_b200 import SamplingConfig, gauss_legendre, plan_alt
+
+import oracle.apply as OA
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(64, [0, 3, 64, 126, 127], 16), (128, [100, 0, 1], 16),
+         (256, [0, 1, 300, 511], 32), (512, [0, 1, 100, 700], 512)]
+
+
+def _run(monkeypatch, mode, plans, flat_f, flat_i, **env):
+    import torch
+    from paper_2004_11346_b200.api import DevicePlan, FORWARD, INVERSE
+    monkeypatch.setenv("BFSHT_CHAIN", str(mode))
+    for k, v in env.items():
+        monkeypatch.setenv(k, str(v))
+    dp = DevicePlan(plans)
+    f = dp.alt_orders(FORWARD, torch.from_numpy(flat_f).cuda()).cpu().numpy()
+    i = dp.alt_orders(INVERSE, torch.from_numpy(flat_i).cuda()).cpu().numpy()
+    n_launch = dp.launches()
+    dp.close()
+    return f, i, n_launch
+
+
+@pytest.mark.parametrize("n,ms,n0", CASES)
+def test_chain_kernel_bitwise_equals_stage_kernel(monkeypatch, n, ms, n0):
+    q = gauss_legendre(2 * n)
+    plans = [plan_alt(n, m, SamplingConfig(tolerance=1e-12), n0=n0, quadrature=q)
+             for m in ms]
+    rng = np.random.default_rng(n)
+    vf = [rng.standard_normal(2 * n - m) + 1j * rng.standard_normal(2 * n - m) for m in ms]
+    vi = [rng.standard_normal(2 * n) + 1j * rng.standard_normal(2 * n) for _ in ms]
+    ff, fi = np.concatenate(vf), np.concatenate(vi)
+    f0, i0, _ = _run(monkeypatch, 0, plans, ff, fi)
+    for mode, env in ((1, {}), (2, {}), (2, {"BFSHT_CHAIN_BUNDLES": 1}),
+                      (1, {"BFSHT_CHAIN_BUNDLES": 64, "BFSHT_CHAIN_CFIX": 0})):
+        f1, i1, _ = _run(monkeypatch, mode, plans, ff, fi, **env)
+        assert np.array_equal(f0, f1), (mode, env)
+        assert np.array_equal(i0, i1), (mode, env)
+    out = f0.reshape(len(ms), 2 * n)
+    pos = 0
+    for o, (p, v, f) in enumerate(zip(plans, vf, vi)):
+        assert np.linalg.norm(out[o] - OA.alt_forward(p, v)) <= 1e-12 * np.linalg.norm(out[o])
+        ln = 2 * n - p.m
+        want = OA.alt_inverse(p, f)
+        assert np.linalg.norm(i0[pos:pos + ln] - want) <= 1e-12 * np.linalg.norm(want)
+        pos += ln
+
+
+def test_chain_kernel_sht_bitwise(monkeypatch):
+    """Whole SHT at N=64 (n0=16: butterflies at every low order) with and
+    without the chain kernel."""
+    import torch
+    from paper_2004_11346_b200 import ShtCoeffs, plan_sht
+    from paper_2004_11346_b200.api import ShtDevice
+    n = 64
+    plan = plan_sht(n, n0=16)
+    rng = np.random.default_rng(5)
+    flat = rng.standard_normal(4 * n * n) + 1j * rng.standard_normal(4 * n * n)
+    res = []
+    for mode in (0, 1, 2):
+        monkeypatch.setenv("BFSHT_CHAIN", str(mode))
+        dev = ShtDevice(plan)
+        g = dev.forward(torch.from_numpy(flat).cuda())
+        b = dev.inverse(g)
+        res.append((g.cpu().numpy(), b.cpu().numpy()))
+    for g, b in res[1:]:
+        assert np.array_equal(g, res[0][0])
+        assert np.array_equal(b, res[0][1])
