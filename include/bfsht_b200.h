@@ -145,6 +145,10 @@ double *bfsht_plan_arena(bfsht_plan *pl);
 int bfsht_alt_apply(bfsht_plan *pl, int dir, void *stream);
 /* One stage of one direction (stages run in order; for profiling). */
 int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream);
+/* Chain schedule of one stage: out[0] = bundles (0: the stage runs on the
+ * stage kernel), out[1] = op records, out[2] = index adds folded into the
+ * preceding tile op's record. */
+int bfsht_plan_chain_info(bfsht_plan *pl, int dir, int stage, int64_t out[3]);
 
 /* Per-order ALT boundary (alt_forward / alt_inverse for one or more plans):
  * in/out are device complex128 buffers laid out plan after plan, lengths

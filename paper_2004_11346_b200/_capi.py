@@ -27,6 +27,8 @@ def declare(lib):
     lib.bfsht_alt_apply.argtypes = [_P, _I, _P]
     lib.bfsht_alt_stage.restype = _I
     lib.bfsht_alt_stage.argtypes = [_P, _I, _I, _P]
+    lib.bfsht_plan_chain_info.restype = _I
+    lib.bfsht_plan_chain_info.argtypes = [_P, _I, _I, ctypes.POINTER(_I64)]
     lib.bfsht_alt_orders.restype = _I
     lib.bfsht_alt_orders.argtypes = [_P, _I, _P, _P, _P, _P]
     lib.bfsht_alt_fields.restype = _I
@@ -87,7 +89,7 @@ EXPORTS = (
     "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
     "bfsht_packed_free", "bfsht_rec_coeffs", "bfsht_regen_tile_host", "bfsht_last_error", "bfsht_plan_upload",
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
-    "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_alt_orders", "bfsht_alt_fields",
+    "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_plan_chain_info", "bfsht_alt_orders", "bfsht_alt_fields",
     "bfsht_half_apply", "bfsht_sht_batch", "bfsht_alt_apply_wide",
     "bfsht_sht_forward", "bfsht_sht_inverse", "bfsht_dft_rows", "bfsht_half_table_device",
     "bfsht_plan_launches",

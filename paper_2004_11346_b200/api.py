@@ -143,6 +143,14 @@ class DevicePlan:
     def launches(self):
         return int(self.lib.bfsht_plan_launches(self.handle))
 
+    def chain_info(self, direction, stage):
+        """(bundles, op records, folded index adds) of one stage's chain
+        schedule; bundles == 0: the stage runs on the stage kernel."""
+        out = (ctypes.c_int64 * 3)()
+        check(self.lib, self.lib.bfsht_plan_chain_info(self.handle, direction, stage, out),
+              "bfsht_plan_chain_info")
+        return tuple(int(v) for v in out)
+
     # -------------------------------------------------------------- apply
     def alt_apply(self, direction, stream=None):
         """All ALT stages over the arena (inputs already in place)."""

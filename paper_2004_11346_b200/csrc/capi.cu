@@ -241,6 +241,24 @@ int bfsht_alt_stage(bfsht_plan *pl, int dir, int stage, void *stream) {
     return bf_run_stage(pl, dir, stage, (cudaStream_t)stream);
 }
 
+int bfsht_plan_chain_info(bfsht_plan *pl, int dir, int stage, int64_t out[3]) {
+    if (!pl || !out || (dir != BFSHT_FORWARD && dir != BFSHT_INVERSE)) {
+        g_err = "bad plan, direction or output";
+        return -1;
+    }
+    out[0] = out[1] = out[2] = 0;
+    if (stage < 0 || stage + 1 >= (int)pl->stages[dir].size()) {
+        g_err = "stage out of range";
+        return -1;
+    }
+    if (stage < (int)pl->chain[dir].size()) {
+        out[0] = pl->chain[dir][stage].nb;
+        out[1] = pl->chain[dir][stage].nrec;
+        out[2] = pl->chain[dir][stage].nfold;
+    }
+    return 0;
+}
+
 int bfsht_alt_orders(bfsht_plan *pl, int dir, const double *in, double *out,
                      const double *weights, void *stream) {
     DeviceGuard guard(pl);

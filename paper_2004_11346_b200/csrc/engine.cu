@@ -176,8 +176,20 @@ struct Cursor {
     int raw;                     // lane 0: claimed id of the task after next
 };
 
+// One claim by lane 0, as inline PTX: with atomicAdd() the compiler applies
+// its warp-aggregation pattern (vote, popc, atomic, shuffle) and the shuffle
+// reads the atomic's result at once — ncu showed the warp stalled there for
+// the whole L2 round trip (6-9% of the chain stages' samples).  This way
+// the result stays in flight until the next bcast() reads it.
+__device__ __forceinline__ int claim_counter(int *counter, int lane) {
+    int v = 0;
+    if (lane == 0)
+        asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(counter) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int claim_raw(const StageArgs &a, int lane) {
-    return lane == 0 ? atomicAdd(a.counter, 1) : 0;
+    return claim_counter(a.counter, lane);
 }
 
 __device__ __forceinline__ int bcast(int raw) { return __shfl_sync(0xffffffffu, raw, 0); }
@@ -846,7 +858,7 @@ struct CStream {
 };
 
 __device__ __forceinline__ int chain_claim(const ChainArgs &a, int lane) {
-    return lane == 0 ? atomicAdd(a.counter, 1) : 0;
+    return claim_counter(a.counter, lane);
 }
 
 // index of the next record of this warp's stream, -1 at the end
@@ -1063,13 +1075,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_chain_kernel(ChainArgs a) 
         if (f & BF_CF_LAST) {
             const int nout = mb.w & 0xff;
             const int stride = (mb.w >> 8) ? (mb.w >> 8) : 1;
+            double *o = a.arena + ((int64_t)mb.z + (int64_t)g * stride) * NR + 2 * q;
+            const int64_t step = (int64_t)stride * (8 * NR);
+            const int lim = q < QACT ? nout - g : 0;   // slot 8j + g < nout
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                const int sl = 8 * j + g;
-                if (q < QACT && sl < nout) {
-                    double *o = a.arena + ((int64_t)mb.z + (int64_t)sl * stride) * NR + 2 * q;
+                if (8 * j < lim)
                     *reinterpret_cast<double2 *>(o) = make_double2(acc[0][j][0], acc[0][j][1]);
-                }
+                o += step;
                 acc[0][j][0] = acc[0][j][1] = 0.0;
             }
         }
@@ -1415,13 +1428,13 @@ static int env_int(const char *name, int dflt) {
 // BFSHT_CHAIN: 0 = every stage on alt_stage_kernel; 1 (default) = stages
 // holding gather / lane-map ops (the butterfly chain; stage 0 also carries
 // the low-rank cores) on alt_chain_kernel; 2 = every stage without
-// regenerated tiles.  BFSHT_CHAIN_BUNDLES: bundles per warp (default 6).
+// regenerated tiles.  BFSHT_CHAIN_BUNDLES: bundles per warp (default 8).
 // BFSHT_CHAIN_CFIX: fixed cost of an op in bytes-equivalents for the bundle
 // balance (default 3072).
 int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
     const int mode = env_int("BFSHT_CHAIN", 1);
     if (!ops || !tasks || mode <= 0) return 0;
-    const int per_warp = std::max(1, env_int("BFSHT_CHAIN_BUNDLES", 6));
+    const int per_warp = std::max(1, env_int("BFSHT_CHAIN_BUNDLES", 8));
     const double cfix = (double)std::max(0, env_int("BFSHT_CHAIN_CFIX", 3072));
     const int64_t W = (int64_t)pl->sm_count * kWarps;
     std::vector<bf_crec> recs;
@@ -1471,6 +1484,7 @@ int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
                             pr.addoff = o.off;
                             pr.add_in = o.in;
                             sp.cost += 32.0 * o.R;
+                            pl->chain[d][s].nfold++;
                             continue;
                         }
                     }
@@ -1523,6 +1537,7 @@ int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
             }
             pl->chain[d][s].b0 = (int64_t)bund.size();
             pl->chain[d][s].nb = nb;
+            pl->chain[d][s].nrec = (int64_t)trec.size();
             for (int i = 0; i < nb; ++i) {
                 bund.push_back((int32_t)recs.size());
                 for (int32_t t : members[i])

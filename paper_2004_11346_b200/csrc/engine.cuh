@@ -59,6 +59,7 @@ struct bfsht_plan {
     struct ChainStage {
         int64_t b0 = 0;               // first entry of the stage in chain_bund
         int nb = 0;                   // bundles
+        int64_t nrec = 0, nfold = 0;  // records, index adds folded into tile ops
     };
     std::vector<ChainStage> chain[2];
     void *chain_rec = nullptr;        // device: bf_crec records, bundle after bundle

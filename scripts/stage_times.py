@@ -52,7 +52,9 @@ for d, bounds in ((0, pk.stages_fwd), (1, pk.stages_inv)):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.reps
+        nb, nrec, nfold = dp.chain_info(d, s)
         rec = {"dir": d, "stage": s, "tasks": t1 - t0, "ops": int(sel.size), "gather_ops": gathers,
+               "chain_bundles": nb, "chain_records": nrec, "folded_adds": nfold,
                "tile_MB": tb / 1e6, "vec_MB": vb / 1e6, "avg_tile_KB": tb / max(sel.size, 1) / 1e3,
                "ms": ms, "tile_GBps": tb / ms / 1e6}
         out.append(rec)
