@@ -115,7 +115,32 @@ int bfsht_regen_tile_host(const double *seed, int R, int C, const double *rec,
                           const double *x_pos, double mag_min, double *out);
 void bfsht_packed_free(bfsht_packed *p);
 
+/* Chain schedule (host side of the chain kernel, csrc/engine.cu): the
+ * stages of one direction that are made of small tasks — the butterfly
+ * factors' gather / scatter tasks (butterfly.py:275-292) and the low-rank
+ * cores (lowrank.py:196-202) — re-encoded as one 32-byte record per op
+ * (csrc/format.h bf_crec; an index add folded into the tile op it follows)
+ * in cost-balanced bundles of whole tasks.  ops / tasks = arrays 1 and 4
+ * of bfsht_packed_arrays, bounds = one direction's stage bounds (nstages +
+ * 1), warps = worker warps of the device (SMs x 12); mode 1 = stages that
+ * hold gather / lane-map ops, 2 = every stage without regenerated tiles,
+ * 0 = none; per_warp = bundles per warp, cfix = fixed cost of an op in byte
+ * equivalents.  bfsht_plan_upload / bfsht_plan_wrap call this themselves;
+ * it is exported for tests and tools. */
+typedef struct bfsht_chain_sched bfsht_chain_sched;
+int bfsht_chain_schedule(const void *ops, const void *tasks, const int64_t *bounds, int nstages,
+                         int warps, int mode, int per_warp, int cfix, bfsht_chain_sched **out);
+/* recs: bf_crec records (nrecs), bund: bundle bounds (record indices; a
+ * stage with nb bundles owns nb + 1 consecutive entries), stage: 4 int64
+ * per stage = first bund entry, bundles (0: not a chain stage), records,
+ * folded index adds. */
+int bfsht_chain_sched_arrays(const bfsht_chain_sched *sc, const void **recs, int64_t *nrecs,
+                             const int32_t **bund, int64_t *nbund, const int64_t **stage);
+void bfsht_chain_sched_free(bfsht_chain_sched *sc);
+
 const char *bfsht_last_error(void);
+/* message of the last failed host-side call (packer, chain schedule) */
+const char *bfsht_host_last_error(void);
 
 /* ------------------------------------------------------------- device side */
 typedef struct bfsht_plan bfsht_plan;       /* opaque device plan */

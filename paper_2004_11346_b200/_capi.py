@@ -87,7 +87,8 @@ def declare(lib):
 # every symbol include/bfsht_b200.h declares (checked by tests on CPU)
 EXPORTS = (
     "bfsht_pack_plan", "bfsht_packed_info", "bfsht_packed_arrays",
-    "bfsht_packed_free", "bfsht_rec_coeffs", "bfsht_regen_tile_host", "bfsht_last_error", "bfsht_plan_upload",
+    "bfsht_packed_free", "bfsht_chain_schedule", "bfsht_chain_sched_arrays",
+    "bfsht_chain_sched_free", "bfsht_host_last_error", "bfsht_rec_coeffs", "bfsht_regen_tile_host", "bfsht_last_error", "bfsht_plan_upload",
     "bfsht_plan_wrap", "bfsht_plan_free", "bfsht_plan_arena",
     "bfsht_alt_apply", "bfsht_alt_stage", "bfsht_plan_chain_info", "bfsht_alt_orders", "bfsht_alt_fields",
     "bfsht_half_apply", "bfsht_sht_batch", "bfsht_alt_apply_wide",

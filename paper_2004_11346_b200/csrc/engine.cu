@@ -34,7 +34,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
-#include <queue>
+#include <string>
 
 #include "engine.cuh"
 #include "recur.h"
@@ -1425,146 +1425,62 @@ static int env_int(const char *name, int dflt) {
     return (v && *v) ? std::atoi(v) : dflt;
 }
 
-// BFSHT_CHAIN: 0 = every stage on alt_stage_kernel; 1 (default) = stages
-// holding gather / lane-map ops (the butterfly chain; stage 0 also carries
-// the low-rank cores) on alt_chain_kernel; 2 = every stage without
-// regenerated tiles.  BFSHT_CHAIN_BUNDLES: bundles per warp (default 8).
-// BFSHT_CHAIN_CFIX: fixed cost of an op in bytes-equivalents for the bundle
+// The schedule itself is built on the host by bfsht_chain_schedule
+// (packer.cpp); this uploads it.  Environment knobs, read when a plan is
+// created: BFSHT_CHAIN = 0 every stage on alt_stage_kernel, 1 (default)
+// stages holding gather / lane-map ops (the butterfly chain; stage 0 also
+// carries the low-rank cores) on alt_chain_kernel, 2 every stage without
+// regenerated tiles; BFSHT_CHAIN_BUNDLES = bundles per warp (default 8);
+// BFSHT_CHAIN_CFIX = fixed cost of an op in byte equivalents for the bundle
 // balance (default 3072).
 int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
     const int mode = env_int("BFSHT_CHAIN", 1);
     if (!ops || !tasks || mode <= 0) return 0;
     const int per_warp = std::max(1, env_int("BFSHT_CHAIN_BUNDLES", 8));
-    const double cfix = (double)std::max(0, env_int("BFSHT_CHAIN_CFIX", 3072));
-    const int64_t W = (int64_t)pl->sm_count * kWarps;
-    std::vector<bf_crec> recs;
-    std::vector<int32_t> bund;
-    struct TaskSpan {
-        int64_t r0;
-        int n;
-        double cost;
-    };
-    std::vector<bf_crec> trec;
-    std::vector<TaskSpan> spans;
+    const int cfix = std::max(0, env_int("BFSHT_CHAIN_CFIX", 3072));
     for (int d = 0; d < 2; ++d) {
         const std::vector<int64_t> &b = pl->stages[d];
         const int nst = (int)b.size() - 1;
         pl->chain[d].assign(nst > 0 ? nst : 0, bfsht_plan::ChainStage());
-        for (int s = 0; s < nst; ++s) {
-            const int64_t t0 = b[s], t1 = b[s + 1];
-            if (t1 <= t0) continue;
-            bool regen = false, small = false;
-            for (int64_t t = t0; t < t1 && !regen; ++t)
-                for (int i = 0; i < tasks[t].op_count; ++i) {
-                    const uint8_t f = ops[tasks[t].op_begin + i].flags;
-                    if (f & BF_OPF_REGEN) regen = true;
-                    if (f & (BF_OPF_GATHER | BF_OPF_LANEMAP)) small = true;
-                }
-            if (regen || (mode == 1 && !small)) continue;
-            trec.clear();
-            spans.clear();
-            for (int64_t t = t0; t < t1; ++t) {
-                const bf_task &tk = tasks[t];
-                TaskSpan sp;
-                sp.r0 = (int64_t)trec.size();
-                sp.cost = 0.0;
-                bool have_prev = false;
-                for (int i = 0; i < tk.op_count; ++i) {
-                    const bf_op &o = ops[tk.op_begin + i];
-                    if (o.tile % 16 != 0 || o.tile / 16 > (int64_t)UINT32_MAX) {
-                        bfsht_set_error("tile offset not representable in a chain record");
-                        return -3;
-                    }
-                    if (o.kind == BF_OP_ADD && (o.flags & BF_OPF_GATHER) && have_prev) {
-                        bf_crec &pr = trec.back();
-                        if (pr.kind != BF_OP_ADD && !(pr.flags & BF_CF_ADD) &&
-                            bf_tile_doubles(pr.R, pr.C) <= BF_FOLD_AT && o.R <= BF_T) {
-                            pr.flags |= BF_CF_ADD;
-                            pr.addR = o.R;
-                            pr.addoff = o.off;
-                            pr.add_in = o.in;
-                            sp.cost += 32.0 * o.R;
-                            pl->chain[d][s].nfold++;
-                            continue;
-                        }
-                    }
-                    bf_crec c;
-                    std::memset(&c, 0, sizeof(c));
-                    c.tile = (uint32_t)(o.tile / 16);
-                    c.in = o.in;
-                    c.aux = o.aux;
-                    c.kind = o.kind;
-                    c.R = o.R;
-                    c.C = o.C;
-                    c.off = o.off;
-                    c.flags = (uint8_t)(o.flags & (BF_OPF_GATHER | BF_OPF_LANEMAP));
-                    trec.push_back(c);
-                    have_prev = true;
-                    sp.cost += cfix + (o.kind == BF_OP_ADD
-                                           ? 32.0 * o.R
-                                           : 8.0 * (double)bf_tile_doubles(o.R, o.C) +
-                                                 32.0 * (o.kind == BF_OP_TILE_N ? o.C : o.R));
-                }
-                if ((int64_t)trec.size() == sp.r0) {
-                    bfsht_set_error("task without ops");
-                    return -3;
-                }
-                bf_crec &last = trec.back();
-                last.flags |= BF_CF_LAST;
-                last.out = tk.out;
-                last.nout = tk.nout;
-                sp.n = (int)((int64_t)trec.size() - sp.r0);
-                spans.push_back(sp);
-            }
-            // LPT: tasks by descending cost onto the least-loaded bundle
-            const int64_t ntasks = t1 - t0;
-            const int nb = (int)std::min<int64_t>(ntasks, W * per_warp);
-            std::vector<int32_t> order(ntasks);
-            for (int64_t i = 0; i < ntasks; ++i) order[i] = (int32_t)i;
-            std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
-                return spans[x].cost > spans[y].cost;
-            });
-            std::vector<std::vector<int32_t>> members(nb);
-            std::priority_queue<std::pair<double, int>, std::vector<std::pair<double, int>>,
-                                std::greater<std::pair<double, int>>>
-                heap;
-            for (int i = 0; i < nb; ++i) heap.push({0.0, i});
-            for (int32_t t : order) {
-                auto top = heap.top();
-                heap.pop();
-                members[top.second].push_back(t);
-                heap.push({top.first + spans[t].cost, top.second});
-            }
-            pl->chain[d][s].b0 = (int64_t)bund.size();
-            pl->chain[d][s].nb = nb;
-            pl->chain[d][s].nrec = (int64_t)trec.size();
-            for (int i = 0; i < nb; ++i) {
-                bund.push_back((int32_t)recs.size());
-                for (int32_t t : members[i])
-                    recs.insert(recs.end(), trec.begin() + spans[t].r0,
-                                trec.begin() + spans[t].r0 + spans[t].n);
-                if ((int64_t)recs.size() > INT32_MAX) {
-                    bfsht_set_error("chain records exceed int32");
-                    return -3;
-                }
-            }
-            bund.push_back((int32_t)recs.size());
+        if (nst <= 0) continue;
+        bfsht_chain_sched *sc = nullptr;
+        if (bfsht_chain_schedule(ops, tasks, b.data(), nst, pl->sm_count * kWarps, mode, per_warp,
+                                 cfix, &sc)) {
+            bfsht_set_error(std::string("chain schedule: ") + bfsht_host_last_error());
+            return -3;
         }
+        const void *recs = nullptr;
+        const int32_t *bund = nullptr;
+        const int64_t *st = nullptr;
+        int64_t nrec = 0, nbund = 0;
+        bfsht_chain_sched_arrays(sc, &recs, &nrec, &bund, &nbund, &st);
+        if (nrec > 0) {
+            void *dr = nullptr, *db = nullptr;
+            if (cudaMalloc(&dr, (size_t)nrec * sizeof(bf_crec)) != cudaSuccess ||
+                cudaMalloc(&db, (size_t)nbund * sizeof(int32_t)) != cudaSuccess ||
+                cudaMemcpy(dr, recs, (size_t)nrec * sizeof(bf_crec), cudaMemcpyHostToDevice) !=
+                    cudaSuccess ||
+                cudaMemcpy(db, bund, (size_t)nbund * sizeof(int32_t), cudaMemcpyHostToDevice) !=
+                    cudaSuccess) {
+                if (dr) cudaFree(dr);
+                if (db) cudaFree(db);
+                bfsht_chain_sched_free(sc);
+                bfsht_set_error("chain schedule upload failed");
+                return -2;
+            }
+            pl->owned.push_back(dr);
+            pl->owned.push_back(db);
+            pl->chain_rec[d] = dr;
+            pl->chain_bund[d] = (int32_t *)db;
+            for (int s = 0; s < nst; ++s) {
+                pl->chain[d][s].b0 = st[4 * s];
+                pl->chain[d][s].nb = (int)st[4 * s + 1];
+                pl->chain[d][s].nrec = st[4 * s + 2];
+                pl->chain[d][s].nfold = st[4 * s + 3];
+            }
+        }
+        bfsht_chain_sched_free(sc);
     }
-    if (recs.empty()) {
-        for (int d = 0; d < 2; ++d)
-            for (auto &c : pl->chain[d]) c.nb = 0;
-        return 0;
-    }
-    BF_CUDA(cudaMalloc(&pl->chain_rec, recs.size() * sizeof(bf_crec)));
-    pl->owned.push_back(pl->chain_rec);
-    BF_CUDA(cudaMemcpy(pl->chain_rec, recs.data(), recs.size() * sizeof(bf_crec),
-                       cudaMemcpyHostToDevice));
-    void *bd = nullptr;
-    BF_CUDA(cudaMalloc(&bd, bund.size() * sizeof(int32_t)));
-    pl->owned.push_back(bd);
-    pl->chain_bund = (int32_t *)bd;
-    BF_CUDA(cudaMemcpy(bd, bund.data(), bund.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     return 0;
 }
 
@@ -1576,8 +1492,8 @@ static int launch_chain(bfsht_plan *pl, int dir, int s, int *counter, cudaStream
     if (rc) return rc;
     ChainArgs a;
     a.tiles = pl->tiles;
-    a.rec = (const int4 *)pl->chain_rec;
-    a.bund = pl->chain_bund + c.b0;
+    a.rec = (const int4 *)pl->chain_rec[dir];
+    a.bund = pl->chain_bund[dir] + c.b0;
     a.idx = pl->idx;
     a.maps = pl->maps;
     a.arena = pl->arena;

@@ -62,8 +62,8 @@ struct bfsht_plan {
         int64_t nrec = 0, nfold = 0;  // records, index adds folded into tile ops
     };
     std::vector<ChainStage> chain[2];
-    void *chain_rec = nullptr;        // device: bf_crec records, bundle after bundle
-    int32_t *chain_bund = nullptr;    // device: bundle bounds (record indices)
+    void *chain_rec[2] = {nullptr, nullptr};        // device, per direction: bf_crec records
+    int32_t *chain_bund[2] = {nullptr, nullptr};    // device: bundle bounds (record indices)
 };
 
 void bfsht_set_error(const std::string &msg);

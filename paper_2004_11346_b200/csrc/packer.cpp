@@ -934,6 +934,154 @@ extern "C" int bfsht_packed_arrays(const bfsht_packed *p, const void *arrays[12]
     return 0;
 }
 
+// ---------------------------------------------------------- chain schedule
+// Re-encodes the stages made of small tasks (butterfly gather / scatter
+// tasks, low-rank cores) for the chain kernel (engine.cu alt_chain_kernel):
+// one 32-byte bf_crec per op, an index add folded into the tile op it
+// follows when that tile leaves the tail of its ring slot free, tasks
+// grouped by LPT into cost-balanced bundles.  Op order inside a task is
+// kept, so the chain kernel's sums are those of the stage kernel.
+struct bfsht_chain_sched {
+    std::vector<bf_crec> recs;
+    std::vector<int32_t> bund;
+    std::vector<int64_t> stage;   // per stage: first bundle entry, bundles, records, folded adds
+};
+
+extern "C" int bfsht_chain_schedule(const void *ops_v, const void *tasks_v, const int64_t *bounds,
+                                    int nstages, int warps, int mode, int per_warp, int cfix,
+                                    bfsht_chain_sched **out) {
+    try {
+        if (!ops_v || !tasks_v || !bounds || !out || nstages < 0 || warps < 1 || per_warp < 1 ||
+            cfix < 0)
+            throw std::runtime_error("bad chain schedule arguments");
+        const bf_op *ops = (const bf_op *)ops_v;
+        const bf_task *tasks = (const bf_task *)tasks_v;
+        auto sc = std::make_unique<bfsht_chain_sched>();
+        sc->stage.assign((size_t)nstages * 4, 0);
+        struct Span {
+            int64_t r0;
+            int n;
+            double cost;
+        };
+        std::vector<bf_crec> trec;
+        std::vector<Span> spans;
+        for (int s = 0; s < nstages && mode > 0; ++s) {
+            const int64_t t0 = bounds[s], t1 = bounds[s + 1];
+            if (t1 <= t0) continue;
+            bool regen = false, small = false;
+            for (int64_t t = t0; t < t1 && !regen; ++t)
+                for (int i = 0; i < tasks[t].op_count; ++i) {
+                    const uint8_t f = ops[tasks[t].op_begin + i].flags;
+                    if (f & BF_OPF_REGEN) regen = true;
+                    if (f & (BF_OPF_GATHER | BF_OPF_LANEMAP)) small = true;
+                }
+            if (regen || (mode == 1 && !small)) continue;
+            trec.clear();
+            spans.clear();
+            int64_t nfold = 0;
+            for (int64_t t = t0; t < t1; ++t) {
+                const bf_task &tk = tasks[t];
+                Span sp;
+                sp.r0 = (int64_t)trec.size();
+                sp.cost = 0.0;
+                for (int i = 0; i < tk.op_count; ++i) {
+                    const bf_op &o = ops[tk.op_begin + i];
+                    if (o.kind != BF_OP_ADD && (o.tile % 16 != 0 || o.tile / 16 > (int64_t)UINT32_MAX))
+                        throw std::runtime_error("tile offset not representable in a chain record");
+                    if (o.kind == BF_OP_ADD && (o.flags & BF_OPF_GATHER) &&
+                        (int64_t)trec.size() > sp.r0) {
+                        bf_crec &pr = trec.back();
+                        if (pr.kind != BF_OP_ADD && !(pr.flags & BF_CF_ADD) &&
+                            bf_tile_doubles(pr.R, pr.C) <= BF_FOLD_AT && o.R <= BF_T) {
+                            pr.flags |= BF_CF_ADD;
+                            pr.addR = o.R;
+                            pr.addoff = o.off;
+                            pr.add_in = o.in;
+                            sp.cost += 32.0 * o.R;
+                            ++nfold;
+                            continue;
+                        }
+                    }
+                    bf_crec c;
+                    std::memset(&c, 0, sizeof(c));
+                    c.tile = o.kind == BF_OP_ADD ? 0u : (uint32_t)(o.tile / 16);
+                    c.in = o.in;
+                    c.aux = o.aux;
+                    c.kind = o.kind;
+                    c.R = o.R;
+                    c.C = o.C;
+                    c.off = o.off;
+                    c.flags = (uint8_t)(o.flags & (BF_OPF_GATHER | BF_OPF_LANEMAP));
+                    trec.push_back(c);
+                    sp.cost += (double)cfix +
+                               (o.kind == BF_OP_ADD ? 32.0 * o.R
+                                                    : 8.0 * (double)bf_tile_doubles(o.R, o.C) +
+                                                          32.0 * (o.kind == BF_OP_TILE_N ? o.C : o.R));
+                }
+                if ((int64_t)trec.size() == sp.r0) throw std::runtime_error("task without ops");
+                bf_crec &last = trec.back();
+                last.flags |= BF_CF_LAST;
+                last.out = tk.out;
+                last.nout = tk.nout;
+                sp.n = (int)((int64_t)trec.size() - sp.r0);
+                spans.push_back(sp);
+            }
+            // LPT: tasks by descending cost onto the least-loaded bundle
+            const int64_t ntasks = t1 - t0;
+            const int nb = (int)std::min<int64_t>(ntasks, (int64_t)warps * per_warp);
+            std::vector<int32_t> order((size_t)ntasks);
+            for (int64_t i = 0; i < ntasks; ++i) order[i] = (int32_t)i;
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int32_t x, int32_t y) { return spans[x].cost > spans[y].cost; });
+            std::vector<std::vector<int32_t>> members((size_t)nb);
+            typedef std::pair<double, int> Load;
+            std::vector<Load> heap;
+            for (int i = 0; i < nb; ++i) heap.push_back({0.0, i});
+            auto cmp = [](const Load &x, const Load &y) { return x > y; };
+            std::make_heap(heap.begin(), heap.end(), cmp);
+            for (int32_t t : order) {
+                std::pop_heap(heap.begin(), heap.end(), cmp);
+                Load &top = heap.back();
+                members[top.second].push_back(t);
+                top.first += spans[t].cost;
+                std::push_heap(heap.begin(), heap.end(), cmp);
+            }
+            sc->stage[4 * s] = (int64_t)sc->bund.size();
+            sc->stage[4 * s + 1] = nb;
+            sc->stage[4 * s + 2] = (int64_t)trec.size();
+            sc->stage[4 * s + 3] = nfold;
+            for (int i = 0; i < nb; ++i) {
+                sc->bund.push_back((int32_t)sc->recs.size());
+                for (int32_t t : members[i])
+                    sc->recs.insert(sc->recs.end(), trec.begin() + spans[t].r0,
+                                    trec.begin() + spans[t].r0 + spans[t].n);
+                if ((int64_t)sc->recs.size() > INT32_MAX)
+                    throw std::runtime_error("chain records exceed int32");
+            }
+            sc->bund.push_back((int32_t)sc->recs.size());
+        }
+        *out = sc.release();
+        return 0;
+    } catch (std::exception &e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+extern "C" int bfsht_chain_sched_arrays(const bfsht_chain_sched *sc, const void **recs,
+                                        int64_t *nrecs, const int32_t **bund, int64_t *nbund,
+                                        const int64_t **stage) {
+    if (!sc) return -1;
+    if (recs) *recs = sc->recs.data();
+    if (nrecs) *nrecs = (int64_t)sc->recs.size();
+    if (bund) *bund = sc->bund.data();
+    if (nbund) *nbund = (int64_t)sc->bund.size();
+    if (stage) *stage = sc->stage.data();
+    return 0;
+}
+
+extern "C" void bfsht_chain_sched_free(bfsht_chain_sched *sc) { delete sc; }
+
 extern "C" int bfsht_rec_coeffs(int64_t m, int64_t k_max, double *out) {
     if (!out || m < 0) return -1;
     for (int64_t k = m; k < k_max; ++k) bfr_coeffs(m, k, &out[2 * (k - m)], &out[2 * (k - m) + 1]);

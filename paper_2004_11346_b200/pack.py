@@ -49,6 +49,15 @@ def declare(lib):
                                           ctypes.c_double, _P]
     lib.bfsht_packed_free.restype = None
     lib.bfsht_packed_free.argtypes = [_P]
+    lib.bfsht_chain_schedule.restype = ctypes.c_int
+    lib.bfsht_chain_schedule.argtypes = [_P, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]
+    lib.bfsht_chain_sched_arrays.restype = ctypes.c_int
+    lib.bfsht_chain_sched_arrays.argtypes = [_P, ctypes.POINTER(_P), ctypes.POINTER(_I64),
+                                             ctypes.POINTER(_P), ctypes.POINTER(_I64),
+                                             ctypes.POINTER(_P)]
+    lib.bfsht_chain_sched_free.restype = None
+    lib.bfsht_chain_sched_free.argtypes = [_P]
     lib.bfsht_host_last_error.restype = ctypes.c_char_p
     lib.bfsht_host_last_error.argtypes = []
 
@@ -68,6 +77,44 @@ INFO_KEYS = ("tile_doubles", "ops", "idx", "maps", "tasks", "arena",
              "dense_blocks", "n", "norders", "free_fwd", "free_inv",
              "regen_tiles", "regen_values", "rec_doubles", "xpos_doubles")
 INFO_LEN = 24
+
+
+CREC_DTYPE = np.dtype([("tile", "<u4"), ("in", "<i4"), ("aux", "<i4"),
+                       ("kind", "u1"), ("R", "u1"), ("C", "u1"), ("off", "u1"),
+                       ("flags", "u1"), ("addR", "u1"), ("addoff", "u1"), ("pad", "u1"),
+                       ("add_in", "<i4"), ("out", "<i4"), ("nout", "<i4")])
+
+
+def chain_schedule(packed, direction, warps=148 * 12, mode=1, per_warp=8, cfix=3072):
+    """Host chain schedule of one direction (include/bfsht_b200.h
+    bfsht_chain_schedule): (records, bundle bounds, per-stage int64 (nst, 4)
+    = first bound entry, bundles, records, folded adds) as numpy copies."""
+    lib = native.host()
+    bounds = np.ascontiguousarray(packed.stages_fwd if direction == 0 else packed.stages_inv)
+    nst = len(bounds) - 1
+    h = _P()
+    rc = lib.bfsht_chain_schedule(packed.ops.ctypes.data, packed.tasks.ctypes.data,
+                                  bounds.ctypes.data, nst, warps, mode, per_warp, cfix,
+                                  ctypes.byref(h))
+    if rc:
+        raise RuntimeError("bfsht_chain_schedule: " + lib.bfsht_host_last_error().decode())
+    try:
+        recs, bund, stage = _P(), _P(), _P()
+        nrec, nbund = _I64(), _I64()
+        lib.bfsht_chain_sched_arrays(h, ctypes.byref(recs), ctypes.byref(nrec),
+                                     ctypes.byref(bund), ctypes.byref(nbund),
+                                     ctypes.byref(stage))
+
+        def copy(ptr, dtype, count):
+            if not count or not ptr.value:
+                return np.zeros(0, dtype=dtype)
+            buf = (ctypes.c_char * (count * np.dtype(dtype).itemsize)).from_address(ptr.value)
+            return np.frombuffer(buf, dtype=dtype, count=count).copy()
+
+        return (copy(recs, CREC_DTYPE, nrec.value), copy(bund, np.int32, nbund.value),
+                copy(stage, np.int64, 4 * nst).reshape(nst, 4))
+    finally:
+        lib.bfsht_chain_sched_free(h)
 
 
 def _addr(a):

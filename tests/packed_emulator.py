@@ -38,9 +38,61 @@ def regen_matrix(pk, off, R, C):
     return buf[((r >> 2) * c4 + (c >> 2)) * 16 + (r & 3) * 4 + (c & 3)]
 
 
-def run_direction(pk, arena, direction):
+CF_LAST, CF_ADD = 8, 16   # format.h bf_crec_flags
+
+
+def run_chain_stage(pk, arena, recs, bund):
+    """One stage from its chain schedule (format.h bf_crec records in
+    bundles; engine.cu alt_chain_kernel): every bundle's records in order,
+    a folded index add right after its tile op, outputs stored on the
+    record flagged last-of-task."""
+    for b in range(len(bund) - 1):
+        acc = np.zeros((SLOTS, NRHS))
+        for r in recs[bund[b]:bund[b + 1]]:
+            kind, R, C, off = int(r["kind"]), int(r["R"]), int(r["C"]), int(r["off"])
+            flags = int(r["flags"])
+            gather = bool(flags & F_GATHER)
+            if kind == OP_ADD:
+                for j in range(R):
+                    src = int(pk.idx[r["in"] + j]) if gather else int(r["in"]) + j
+                    if src >= 0:
+                        acc[off + j] += arena[src]
+            else:
+                a = tile_matrix(pk, int(r["tile"]) * 16, R, C)
+                nin = C if kind == OP_N else R
+                src = pk.idx[r["in"]:r["in"] + nin] if gather \
+                    else np.arange(r["in"], r["in"] + nin)
+                v = arena[src]
+                res = a @ v if kind == OP_N else a.T @ v
+                width = res.shape[0]
+                for slot in range(SLOTS):
+                    if flags & F_LANEMAP:
+                        sl = int(pk.maps[int(r["aux"]) * SLOTS + slot])
+                    else:
+                        sl = slot - off
+                    if 0 <= sl < width:
+                        acc[slot] += res[sl]
+                if flags & CF_ADD:
+                    for j in range(int(r["addR"])):
+                        src = int(pk.idx[r["add_in"] + j])
+                        if src >= 0:
+                            acc[int(r["addoff"]) + j] += arena[src]
+            if flags & CF_LAST:
+                nout = int(r["nout"]) & 0xFF
+                stride = (int(r["nout"]) >> 8) or 1
+                arena[r["out"] + stride * np.arange(nout)] = acc[:nout]
+                acc[:] = 0.0
+
+
+def run_direction(pk, arena, direction, chain=None):
+    """chain = (records, bundle bounds, per-stage info) from
+    pack.chain_schedule: the stages it covers run from their records."""
     bounds = pk.stages_fwd if direction == 0 else pk.stages_inv
     for s in range(len(bounds) - 1):
+        if chain is not None and chain[2][s, 1] > 0:
+            b0, nb = int(chain[2][s, 0]), int(chain[2][s, 1])
+            run_chain_stage(pk, arena, chain[0], chain[1][b0:b0 + nb + 1])
+            continue
         for t in pk.tasks[bounds[s]:bounds[s + 1]]:
             acc = np.zeros((SLOTS, NRHS))
             for op in pk.ops[t["op_begin"]:t["op_begin"] + t["op_count"]]:
