@@ -494,7 +494,7 @@ def run_ours(args):
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak,
                 "unit": "GB/s", "frac": achieved / peak,
                 "traffic": measured_traffic(n, world, args.regen),
-                "kernel": "alt_stage_kernel (all ALT stages of one direction)",
+                "kernel": "alt_stage_kernel + alt_chain_kernel (all ALT stages of one direction)",
                 "alt_fwd_ms": alt["fwd_ms"], "alt_inv_ms": alt["inv_ms"],
                 "alg_bytes_per_direction": alt_bytes_all / world,
                 "peak_source": f"{peak_kind} MEASURED_PEAKS.json hbm_gbs"}

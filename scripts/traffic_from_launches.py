@@ -13,6 +13,7 @@ The first forward direction is the first run of consecutive ALT launches
 inverse the first run that ends in a coef_unpack launch."""
 import csv
 import json
+import re
 import sys
 
 path = sys.argv[1]
@@ -72,7 +73,9 @@ def summarize(ids):
 
 fwd = alt_run("coef_pack", None)
 inv = alt_run(None, "coef_unpack")
-out = {"source": f"{path} (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
+m = re.search(r"_n(\d+)", path)
+out = {"n": int(m.group(1)) if m else None,
+       "source": f"{path} (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,"
                  "dram__bytes_write.sum --clock-control none; scripts/traffic_from_launches.py)",
        "fwd": summarize(fwd), "inv": summarize(inv)}
 out["traffic_bytes_per_direction"] = (out["fwd"]["traffic_bytes"] + out["inv"]["traffic_bytes"]) / 2
