@@ -198,6 +198,20 @@ class ChunkedSht:
         e1.record()
         self._events.append((key, e0, e1))
 
+    def _warm_dft(self, key, fn):
+        """First launch of a DFT-stage kernel in this process, on one row
+        pair and outside the timed events: the runtime loads the kernel's
+        code lazily, and that host-side pause (about 25 ms for the analysis
+        kernel, seen as a 34 ms analysis stage at N=4096 against 8.5 ms
+        alone) otherwise sits between the stage's two events.  The timed call
+        that follows writes the same rows again."""
+        done = self.__dict__.setdefault("_dft_warm", set())
+        if key in done:
+            return
+        fn()
+        self.torch.cuda.synchronize()
+        done.add(key)
+
     def _collect(self):
         self.torch.cuda.synchronize()
         out = {}
@@ -259,6 +273,9 @@ class ChunkedSht:
         free, total = torch.cuda.mem_get_info(self.device)
         rep["gpu_mem_used_gb"] = (total - free) / 1e9
         st = self._stream()
+        self._warm_dft("synth", lambda: check(lib, lib.bfsht_synth_rows(
+            self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, 1, _ptr(grid), st),
+            "bfsht_synth_rows"))
         self._timed("dft", lambda: check(lib, lib.bfsht_synth_rows(
             self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, n, _ptr(grid), st),
             "bfsht_synth_rows"))
@@ -273,6 +290,9 @@ class ChunkedSht:
         n = self.n
         self._events = []
         st = self._stream()
+        self._warm_dft("anal", lambda: check(lib, lib.bfsht_anal_rows(
+            self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, 1, _ptr(grid),
+            _ptr(self.weights), st), "bfsht_anal_rows"))
         self._timed("dft", lambda: check(lib, lib.bfsht_anal_rows(
             self.ctx.handle, _ptr(self.layout_dev), _ptr(self.ybuf), 0, n, _ptr(grid),
             _ptr(self.weights), st), "bfsht_anal_rows"))

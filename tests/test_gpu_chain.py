@@ -75,3 +75,36 @@ def test_chain_kernel_sht_bitwise(monkeypatch):
     for g, b in res[1:]:
         assert np.array_equal(g, res[0][0])
         assert np.array_equal(b, res[0][1])
+
+
+def test_chain_kernel_with_regenerated_tiles(monkeypatch):
+    """Plans with regenerated turning tiles (f1): mode 2 must leave the
+    stages that hold seeded tiles on the stage kernel; results bitwise those
+    of the stage kernel alone."""
+    import torch
+    from paper_2004_11346_b200.api import DevicePlan, FORWARD, INVERSE
+    n, ms = 256, [0, 1, 300]
+    q = gauss_legendre(2 * n)
+    plans = [plan_alt(n, m, SamplingConfig(tolerance=1e-12), n0=32, quadrature=q) for m in ms]
+    rng = np.random.default_rng(3)
+    ff = np.concatenate([rng.standard_normal(2 * n - m) + 1j * rng.standard_normal(2 * n - m)
+                         for m in ms])
+    fi = np.concatenate([rng.standard_normal(2 * n) + 1j * rng.standard_normal(2 * n)
+                         for _ in ms])
+    res = []
+    for mode in (0, 1, 2):
+        monkeypatch.setenv("BFSHT_CHAIN", str(mode))
+        dp = DevicePlan(plans, regen=1.0)
+        assert dp.packed.regen_tiles > 0
+        nst = len(dp.packed.stages_fwd) - 1
+        info = [dp.chain_info(FORWARD, s) for s in range(nst)]
+        if mode == 0:
+            assert all(i[0] == 0 for i in info)
+        else:
+            assert any(i[0] > 0 for i in info)
+        f = dp.alt_orders(FORWARD, torch.from_numpy(ff).cuda()).cpu().numpy()
+        i = dp.alt_orders(INVERSE, torch.from_numpy(fi).cuda()).cpu().numpy()
+        res.append((f, i))
+        dp.close()
+    for f, i in res[1:]:
+        assert np.array_equal(f, res[0][0]) and np.array_equal(i, res[0][1])
