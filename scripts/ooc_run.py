@@ -187,7 +187,7 @@ def main():
     lay = run.layout
     ms = np.arange(2 * n)
     errs = []
-    for r in [int(v) for v in args.rows.split(",") if v]:
+    for r in sorted({min(int(v), n - 1) for v in args.rows.split(",") if v}):
         spec = np.zeros((2, L), dtype=np.complex128)   # rows n+r, n-1-r
         ent = np.zeros((2, 2 * n, 4))
         for par in range(2):
