@@ -27,6 +27,12 @@
 //    DMMA + 40 fragment loads instead of ~650 scalar instructions, which is
 //    what keeps the kernel on the HBM roofline rather than issue-bound.
 //    Payload bytes are read from HBM exactly once per direction.
+//
+// Kernels in this file: alt_stage_kernel (the model above; final dense /
+// group stages, and every stage of a plan without a chain schedule),
+// alt_chain_kernel (the butterfly-chain and low-rank-core stages from the
+// plan's chain schedule: 32-byte records, bundles, folded index adds — same
+// ring, same sums), alt_group_kernel (batched fields, 4 warps share a ring).
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
