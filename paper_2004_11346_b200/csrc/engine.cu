@@ -894,14 +894,25 @@ __device__ __forceinline__ int chain_gsrc(const ChainArgs &a, const CRec &r, int
     return lane < nvec ? __ldg(a.idx + r.a.y + lane) : -1;
 }
 
-__device__ __forceinline__ int chain_gadd(const ChainArgs &a, const CRec &r, int lane) {
-    if (!(r.b.x & BF_CF_ADD)) return -1;
+// sources of the folded index add: entries lane and lane + 32 (a fold holds
+// up to 64 entries: two back-to-back adds of one scatter task)
+__device__ __forceinline__ int2 chain_gadd(const ChainArgs &a, const CRec &r, int lane) {
+    int2 v = make_int2(-1, -1);
+    if (!(r.b.x & BF_CF_ADD)) return v;
     const int addR = ((uint32_t)r.b.x >> 8) & 0xff;
-    return lane < addR ? __ldg(a.idx + r.b.y + lane) : -1;
+    if (lane < addR) v.x = __ldg(a.idx + r.b.y + lane);
+    if (lane + 32 < addR) v.y = __ldg(a.idx + r.b.y + lane + 32);
+    return v;
+}
+
+// where a fold's entries land in the tile slot: the last 1 KB, or the last
+// 2 KB when it holds more than 32 entries
+__device__ __forceinline__ int fold_at(int addR) {
+    return addR > BF_T ? BF_FOLD_AT - BF_T * BF_NRHS : BF_FOLD_AT;
 }
 
 __device__ __forceinline__ void chain_issue(const ChainArgs &a, ChainRing &ring, int s,
-                                            const CRec &r, int gsrc, int gadd, int lane) {
+                                            const CRec &r, int gsrc, int2 gadd, int lane) {
     const uint32_t w = (uint32_t)r.a.w, f = (uint32_t)r.b.x;
     const int kind = w & 0xff, R = (w >> 8) & 0xff, C = (w >> 16) & 0xff;
     const bool gather = (f & BF_OPF_GATHER) != 0;
@@ -924,14 +935,26 @@ __device__ __forceinline__ void chain_issue(const ChainArgs &a, ChainRing &ring,
         }
     }
     if (f & BF_CF_ADD) {
-        double *d = ring.tile[s] + BF_FOLD_AT + lane * BF_NRHS;
-        if (gadd >= 0) {
-            const double *gp = a.arena + (int64_t)gadd * BF_NRHS;
+        const int addR = (f >> 8) & 0xff;
+        double *d = ring.tile[s] + fold_at(addR) + lane * BF_NRHS;
+        if (gadd.x >= 0) {
+            const double *gp = a.arena + (int64_t)gadd.x * BF_NRHS;
             cp_async16(d, gp);
             cp_async16(d + 2, gp + 2);
         } else {
             *reinterpret_cast<double2 *>(d) = make_double2(0.0, 0.0);
             *reinterpret_cast<double2 *>(d + 2) = make_double2(0.0, 0.0);
+        }
+        if (addR > BF_T) {
+            d += BF_T * BF_NRHS;
+            if (gadd.y >= 0) {
+                const double *gp = a.arena + (int64_t)gadd.y * BF_NRHS;
+                cp_async16(d, gp);
+                cp_async16(d + 2, gp + 2);
+            } else {
+                *reinterpret_cast<double2 *>(d) = make_double2(0.0, 0.0);
+                *reinterpret_cast<double2 *>(d + 2) = make_double2(0.0, 0.0);
+            }
         }
     }
     cp_async_arrive(&ring.full[s]);
@@ -980,7 +1003,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_chain_kernel(ChainArgs a) 
     int i0 = chain_next(a, cs, lane);
     if (i0 >= 0) r0 = load_crec(a, i0);
     int g0 = i0 >= 0 ? chain_gsrc(a, r0, lane) : -1;
-    int ga0 = i0 >= 0 ? chain_gadd(a, r0, lane) : -1;
+    int2 ga0 = i0 >= 0 ? chain_gadd(a, r0, lane) : make_int2(-1, -1);
     int i1 = i0 >= 0 ? chain_next(a, cs, lane) : -1;
     if (i1 >= 0) r1 = load_crec(a, i1);
     uint32_t seq_issue = 0, seq_use = 0;
@@ -1066,7 +1089,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_chain_kernel(ChainArgs a) 
             if (f & BF_CF_ADD) {
                 // folded index add: entry jj adds into slot addoff + jj
                 const int addR = (f >> 8) & 0xff, addoff = (f >> 16) & 0xff;
-                const double *A = ring.tile[s] + BF_FOLD_AT;
+                const double *A = ring.tile[s] + fold_at(addR);
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int jj = 8 * j + g - addoff;

@@ -96,7 +96,9 @@ typedef struct {
  * consecutive; tasks are grouped in cost-balanced bundles that warps
  * claim.  An index add that directly follows a tile op of its task rides
  * on that op's record ("folded": BF_CF_ADD, add_in / addR / addoff), when
- * the tile leaves the last BF_T entries of its ring slot free. */
+ * the tile leaves the last BF_T entries of its ring slot free; a second add
+ * that continues the first (next sources, next slots) extends the fold to
+ * up to 2 BF_T entries when the tile leaves twice that free. */
 enum bf_crec_flags {
     BF_CF_LAST = 8,      /* last op of its task: store the outputs */
     BF_CF_ADD = 16       /* folded index add (gathered through idx[add_in + j]) */

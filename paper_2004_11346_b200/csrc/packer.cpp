@@ -1001,6 +1001,19 @@ extern "C" int bfsht_chain_schedule(const void *ops_v, const void *tasks_v, cons
                             ++nfold;
                             continue;
                         }
+                        // a second add right behind a folded one (the two
+                        // 32-lane adds of a 64-slot scatter task) extends the
+                        // fold when it continues it — next sources, next
+                        // slots — and the tile leaves 2 KB of its slot free
+                        if (pr.kind != BF_OP_ADD && (pr.flags & BF_CF_ADD) && pr.addR == BF_T &&
+                            o.in == pr.add_in + pr.addR && (int)o.off == (int)pr.addoff + pr.addR &&
+                            (int)pr.addR + o.R <= 2 * BF_T &&
+                            bf_tile_doubles(pr.R, pr.C) <= BF_FOLD_AT - BF_T * BF_NRHS) {
+                            pr.addR = (uint8_t)(pr.addR + o.R);
+                            sp.cost += 32.0 * o.R;
+                            ++nfold;
+                            continue;
+                        }
                     }
                     bf_crec c;
                     std::memset(&c, 0, sizeof(c));
