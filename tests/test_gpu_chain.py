@@ -108,3 +108,55 @@ def test_chain_kernel_with_regenerated_tiles(monkeypatch):
         dp.close()
     for f, i in res[1:]:
         assert np.array_equal(f, res[0][0]) and np.array_equal(i, res[0][1])
+
+
+def test_plan_upload_path_builds_the_chain_schedule():
+    """The C-only residency path (bfsht_plan_upload: the library owns every
+    device array) builds the same chain schedule as bfsht_plan_wrap and gives
+    the same results, bit for bit."""
+    import ctypes
+    import torch
+    from paper_2004_11346_b200 import native
+    from paper_2004_11346_b200._capi import check
+    from paper_2004_11346_b200.api import DevicePlan, FORWARD, INVERSE
+    from paper_2004_11346_b200.pack import pack_plans
+    n, ms = 256, [0, 1, 300]
+    q = gauss_legendre(2 * n)
+    plans = [plan_alt(n, m, SamplingConfig(tolerance=1e-12), n0=32, quadrature=q) for m in ms]
+    rng = np.random.default_rng(11)
+    ff = np.concatenate([rng.standard_normal(2 * n - m) + 1j * rng.standard_normal(2 * n - m)
+                         for m in ms])
+    fi = np.concatenate([rng.standard_normal(2 * n) + 1j * rng.standard_normal(2 * n)
+                         for _ in ms])
+    dp = DevicePlan(plans)
+    want_f = dp.alt_orders(FORWARD, torch.from_numpy(ff).cuda()).cpu().numpy()
+    want_i = dp.alt_orders(INVERSE, torch.from_numpy(fi).cuda()).cpu().numpy()
+    nst = len(dp.packed.stages_fwd) - 1
+    want_info = [dp.chain_info(FORWARD, s) for s in range(nst)]
+    assert any(i[0] > 0 for i in want_info)
+
+    lib = native.cuda()
+    packed = pack_plans(plans)
+    h = ctypes.c_void_p()
+    check(lib, lib.bfsht_plan_upload(packed._h, ctypes.byref(h)), "bfsht_plan_upload")
+    try:
+        out = (ctypes.c_int64 * 3)()
+        for s in range(nst):
+            check(lib, lib.bfsht_plan_chain_info(h, FORWARD, s, out), "bfsht_plan_chain_info")
+            assert tuple(int(v) for v in out) == want_info[s]
+        st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        x = torch.from_numpy(ff).cuda()
+        y = torch.empty(len(ms) * 2 * n, dtype=torch.complex128, device="cuda")
+        check(lib, lib.bfsht_alt_orders(h, FORWARD, ctypes.c_void_p(x.data_ptr()),
+                                        ctypes.c_void_p(y.data_ptr()), None, st), "fwd")
+        g = torch.from_numpy(fi).cuda()
+        b = torch.empty(ff.size, dtype=torch.complex128, device="cuda")
+        check(lib, lib.bfsht_alt_orders(h, INVERSE, ctypes.c_void_p(g.data_ptr()),
+                                        ctypes.c_void_p(b.data_ptr()),
+                                        ctypes.c_void_p(dp.weights.data_ptr()), st), "inv")
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), want_f)
+        assert np.array_equal(b.cpu().numpy(), want_i)
+    finally:
+        lib.bfsht_plan_free(h)
+        dp.close()
