@@ -38,6 +38,22 @@ constexpr int kMaxRadix = 24;
 #define BF_DFT_THREADS 256
 #endif
 constexpr int kDftThreads = BF_DFT_THREADS;
+#ifndef BF_DFT_MINBLOCKS
+#define BF_DFT_MINBLOCKS 2
+#endif
+// The row-pair kernels with the row in shared memory (N <= 1024: 64 KB rows)
+// run three CTAs of 128 threads per SM: measured at N=1024 against two CTAs
+// of 256 threads, synthesis 0.162 -> 0.152 ms, analysis 0.191 -> 0.171 ms
+// (more rows in flight hide the global load / store phases; 160 x 3 gave
+// 0.149 / 0.185, 192 x 3 and 224 x 3 spill and are slower).  The L2-scratch
+// kernels keep 256 x 2 (128 x 3 there: N=4096 10.5 / 9.4 vs 9.3 / 8.5 ms).
+#ifndef BF_PAIR_THREADS
+#define BF_PAIR_THREADS 128
+#endif
+#ifndef BF_PAIR_MINBLOCKS
+#define BF_PAIR_MINBLOCKS 3
+#endif
+constexpr int kPairThreads = BF_PAIR_THREADS;
 // shared-memory ceiling of a one-row CTA: two CTAs per SM (228 KB per SM,
 // 1 KB reserved per CTA)
 constexpr int kPairSmemMax = 113 * 1024;
@@ -439,7 +455,7 @@ __device__ __forceinline__ double2 *dft_buffer(double2 *scratch, int rows, int L
 
 // ---- standalone batched DFT: rows of length L (numpy fft / L*ifft)
 template <bool SM, bool GEN>
-__global__ void __launch_bounds__(kDftThreads, 2) dft_rows_kernel(
+__global__ void __launch_bounds__(kDftThreads, BF_DFT_MINBLOCKS) dft_rows_kernel(
     DftDesc d, const double2 *__restrict__ in, double2 *__restrict__ out, int64_t rows,
     const int *__restrict__ perm, const double2 *__restrict__ W, bool inv, bool use_smem,
     double2 *scratch, const double2 *__restrict__ chirp, const double2 *__restrict__ H) {
@@ -478,7 +494,7 @@ __global__ void __launch_bounds__(kDftThreads, 2) dft_rows_kernel(
 // writes the weighted fold (alt.py:239-253).  Twiddle tables are read
 // through L1.  One cluster per row pair, grid = 2 * rows.
 template <bool GEN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, BF_PAIR_MINBLOCKS)
     sht_synth_pair_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
                           const double *__restrict__ arena, int r_count,
                           const double2 *__restrict__ tw, const int *__restrict__ perm,
@@ -583,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
 // CTA, persistent over the rows — the path of rows too long for shared
 // memory (N >= 2048), at 128 registers so two CTAs share an SM.
 template <bool SM, bool GEN>
-__global__ void __launch_bounds__(kDftThreads, 2)
+__global__ void __launch_bounds__(kDftThreads, BF_DFT_MINBLOCKS)
     sht_synth_row_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
                          const double *__restrict__ arena, int r_count,
                          const double2 *__restrict__ tw, const int *__restrict__ perm,
@@ -687,7 +703,8 @@ __global__ void __launch_bounds__(kDftThreads, 2)
 // global memory after the cluster barrier (release / acquire at cluster
 // scope orders those accesses).
 template <bool SM, bool GEN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDftThreads, 2)
+__global__ void __cluster_dims__(2, 1, 1)
+    __launch_bounds__(SM ? kPairThreads : kDftThreads, SM ? BF_PAIR_MINBLOCKS : BF_DFT_MINBLOCKS)
     sht_anal_pair_kernel(DftDesc d, int n, const bf_half *__restrict__ halves,
                          double *__restrict__ arena, const double2 *__restrict__ tw,
                          const int *__restrict__ perm, const double2 *__restrict__ W,
@@ -1177,7 +1194,7 @@ static int launch_synth(bfsht_plan *pl, const bf_half *halves, const double *are
         auto kern = pl->dft_gen ? sht_synth_pair_kernel<true> : sht_synth_pair_kernel<false>;
         int rc = bf_ensure_smem((const void *)kern, smem);
         if (rc) return rc;
-        kern<<<2 * r_count, kDftThreads, smem, st>>>(d, n, halves, arena, r_count, tw,
+        kern<<<2 * r_count, kPairThreads, smem, st>>>(d, n, halves, arena, r_count, tw,
                                                      pl->dft_perm, W, g, yr, ystride, ew, chirp, H);
     } else {
         auto kern = pl->dft_gen ? sht_synth_row_kernel<false, true>
@@ -1214,7 +1231,7 @@ static int launch_anal(bfsht_plan *pl, const bf_half *halves, double *arena, int
     const int nblk = sm ? 2 * r_count : scratch_grid(pl, r_count);
     int rc = bf_ensure_smem((const void *)kern, smem);
     if (rc) return rc;
-    kern<<<nblk, kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g, weights,
+    kern<<<nblk, sm ? kPairThreads : kDftThreads, smem, st>>>(d, n, halves, arena, tw, pl->dft_perm, W, g, weights,
                                           r_begin, r_count, node_y, ew, chirp, H,
                                           reinterpret_cast<double2 *>(pl->dft_scratch));
     BF_CUDA(cudaGetLastError());
