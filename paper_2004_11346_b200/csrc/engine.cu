@@ -128,6 +128,17 @@ __device__ __forceinline__ void cp_async_arrive(unsigned long long *bar) {
                  : "memory");
 }
 
+// Programmatic dependent launch (the ALT stages of one direction are chained
+// with cudaLaunchAttributeProgrammaticStreamSerialization): a stage's CTAs may
+// start as the previous stage's CTAs retire, run their prologue (ring setup,
+// first claims, first record / task loads — all plan data the previous stage
+// does not write) and wait here before they touch the vector arena.  Without
+// the launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -693,6 +704,8 @@ __global__ void __launch_bounds__(Width<NR>::WARPS * 32, 1) alt_stage_kernel(Sta
         g0 = gather_src(a, q0, lane);
         q1 = advance(a, cur, lane);
     };
+    pdl_launch_dependents();
+    pdl_wait();
     while (q0.valid && seq_issue - seq_use < kStages) issue_next();
 
     // task accumulator: acc[grp][j] = slot 8j + lane/4, RHS 8grp + 2(lane%4)
@@ -1019,6 +1032,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) alt_chain_kernel(ChainArgs a) 
             if (i1 >= 0) r1 = load_crec(a, i1);
         }
     };
+    pdl_launch_dependents();
+    pdl_wait();
     while (i0 >= 0 && seq_issue - seq_use < kStages) issue_next();
 
     double acc[1][8][2];
@@ -1427,9 +1442,36 @@ int bf_alt_apply_group(bfsht_plan *pl, int dir, double *arena, cudaStream_t st) 
 
 // reset: zero the stage's task counter first (single-stage calls); the
 // whole-direction paths zero every stage counter with one memset instead
+// One ALT kernel launch; pdl = programmatic dependent launch on the previous
+// kernel in the stream (an ALT stage of the same direction).
+static cudaError_t launch_alt(const void *kern, int grid, int block, size_t smem, cudaStream_t st,
+                              void *args_struct, bool pdl) {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void *args[1] = {args_struct};
+    return cudaLaunchKernelExC(&cfg, kern, args);
+}
+
+static bool pdl_enabled() {
+    static const int on = [] {
+        const char *v = std::getenv("BFSHT_PDL");
+        return (v && *v) ? std::atoi(v) : 1;
+    }();
+    return on != 0;
+}
+
 template <int NR>
 static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, double *arena,
-                        cudaStream_t st, int max_ctas, bool reset) {
+                        cudaStream_t st, int max_ctas, bool reset, bool pdl = false) {
     constexpr int W = Width<NR>::WARPS;
     const size_t smem = sizeof(WarpRing<NR>) * W;
     int rc = bf_ensure_smem((const void *)alt_stage_kernel<NR>, (int)smem);
@@ -1451,8 +1493,7 @@ static int launch_stage(bfsht_plan *pl, int64_t t0, int64_t t1, int *counter, do
     int64_t want = (a.ntasks + W - 1) / W;
     const int cap = (max_ctas > 0 && max_ctas < pl->sm_count) ? max_ctas : pl->sm_count;
     int grid = (int)(want < cap ? want : cap);
-    alt_stage_kernel<NR><<<grid, W * 32, smem, st>>>(a);
-    BF_CUDA(cudaGetLastError());
+    BF_CUDA(launch_alt((const void *)alt_stage_kernel<NR>, grid, W * 32, smem, st, &a, pdl));
     pl->launches += 1;
     return 0;
 }
@@ -1523,7 +1564,7 @@ int bf_chain_build(bfsht_plan *pl, const bf_op *ops, const bf_task *tasks) {
 }
 
 static int launch_chain(bfsht_plan *pl, int dir, int s, int *counter, cudaStream_t st,
-                        bool reset) {
+                        bool reset, bool pdl = false) {
     const bfsht_plan::ChainStage &c = pl->chain[dir][s];
     const size_t smem = sizeof(ChainRing) * kWarps;
     int rc = bf_ensure_smem((const void *)alt_chain_kernel, (int)smem);
@@ -1540,8 +1581,7 @@ static int launch_chain(bfsht_plan *pl, int dir, int s, int *counter, cudaStream
     if (reset) BF_CUDA(cudaMemsetAsync(counter, 0, sizeof(int), st));
     const int64_t want = ((int64_t)c.nb + kWarps - 1) / kWarps;
     const int grid = (int)(want < pl->sm_count ? want : pl->sm_count);
-    alt_chain_kernel<<<grid, kWarps * 32, smem, st>>>(a);
-    BF_CUDA(cudaGetLastError());
+    BF_CUDA(launch_alt((const void *)alt_chain_kernel, grid, kWarps * 32, smem, st, &a, pdl));
     pl->launches += 1;
     return 0;
 }
@@ -1585,13 +1625,17 @@ int bf_alt_apply(bfsht_plan *pl, int dir, cudaStream_t st) {
         return -3;
     }
     BF_CUDA(cudaMemsetAsync(pl->counters, 0, sizeof(int) * nst, st));
+    bool first = true;
     for (int s = 0; s < nst; ++s) {
         if (b[s + 1] <= b[s]) continue;
+        // every stage after the first follows an ALT kernel in the stream
+        const bool pdl = !first && pdl_enabled();
         int rc = is_chain_stage(pl, dir, s)
-                     ? launch_chain(pl, dir, s, pl->counters + s, st, false)
+                     ? launch_chain(pl, dir, s, pl->counters + s, st, false, pdl)
                      : launch_stage<BF_NRHS>(pl, b[s], b[s + 1], pl->counters + s, pl->arena, st,
-                                             0, false);
+                                             0, false, pdl);
         if (rc) return rc;
+        first = false;
     }
     return 0;
 }
